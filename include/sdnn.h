@@ -1,0 +1,145 @@
+/*
+ * sdnn.h -- C ABI of libsdnn.so, the B200 (sm_100a) Sparse DNN inference
+ * engine.  Plain pointers and sizes only; the caller owns every host buffer,
+ * a handle owns its device memory.
+ *
+ * The reference (sdnnbench, /root/reference/pkg/src/sdnnbench) has no FFI:
+ * its boundary is the Python functions below, so each entry point names the
+ * reference function it replaces.  The Python mirror
+ * (paper_1909_05631_b200/engine.py) binds them with ctypes; INTEGRATION.md
+ * shows the binding a reference maintainer would add.
+ *
+ *   reference                                   this ABI
+ *   engine.infer            engine.py:300-324   sdnn_net_* + sdnn_infer
+ *   engine.infer_timed      engine.py:327-340   sdnn_batch_upload + sdnn_run
+ *                                               (+ sdnn_result_device_ms)
+ *   engine._run_layers      engine.py:192-203   sdnn_run (all L layers on device)
+ *   engine.spmm             engine.py:163-175   sdnn_spmm
+ *   engine.apply_bias_relu_clamp  engine.py:178-184  sdnn_bias_relu_clamp
+ *   challenge.categorize    challenge.py:60-67  sdnn_result_categories
+ *   NetworkModel/LayerWeights model.py:128-162  sdnn_net_add_layer_csr
+ *   FeatureBatch result     engine.py:158-160,324  sdnn_result_y_csr
+ *
+ * Return codes map onto the reference's exception classes
+ * (errors.py:12,46,50):  0 ok, 2 ParameterError, 3 CapacityError (also any
+ * CUDA failure), 4 ShapeError.  sdnn_last_error() gives the message of the
+ * calling thread's last failure.
+ *
+ * Threading: distinct handles may be used concurrently from different host
+ * threads (one handle per GPU is the data-parallel layout); one handle must
+ * not be used by two threads at once.
+ */
+#ifndef SDNN_H
+#define SDNN_H
+
+#include <stdint.h>
+
+#include "sdnn_gen.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SDNN_OK 0
+#define SDNN_ERR_PARAMETER 2
+#define SDNN_ERR_CAPACITY 3
+#define SDNN_ERR_SHAPE 4
+
+#define SDNN_F32 0 /* activations and weights stored/computed in float  */
+#define SDNN_F64 1 /* float64: bit-exact with the reference engine      */
+
+typedef struct sdnn_net sdnn_net;       /* device-resident network      */
+typedef struct sdnn_batch sdnn_batch;   /* device-resident input Y0     */
+typedef struct sdnn_result sdnn_result; /* outputs of one run           */
+
+int sdnn_version(void);
+const char *sdnn_last_error(void);
+int sdnn_device_count(int *n);
+
+/* A network of n_neurons x n_neurons layers on CUDA device `device`. */
+int sdnn_net_create(int device, int dtype, int64_t n_neurons, sdnn_net **out);
+void sdnn_net_destroy(sdnn_net *net);
+
+/* Append one layer given as the reference's LayerWeights: CSR by input row
+ * (model.py:51-125: row_offsets[n+1], col_indices[nnz] ascending per row,
+ * values[nnz]) and its scalar bias.  Converted once to the device layout
+ * (ELL by output column, inputs ascending).  Untimed, like model loading
+ * in the reference (engine.py:329-332). */
+int sdnn_net_add_layer_csr(sdnn_net *net, const int64_t *w_off, const int64_t *w_cols,
+                           const double *w_vals, int64_t nnz, double bias);
+
+/* Append one layer already in ELL-by-output form: idx[j*width + s] is the
+ * s-th smallest input feeding output j, vals likewise (n*width each). */
+int sdnn_net_add_layer_ell(sdnn_net *net, int32_t width, const int32_t *idx,
+                           const double *vals, double bias);
+
+/* Generate `count` perm-union layers (sdnn_gen_permunion_ell) with `threads`
+ * host threads and append them, every slot holding `value`. */
+int sdnn_net_add_layers_permunion(sdnn_net *net, uint64_t seed, int64_t first_layer,
+                                  int64_t count, int32_t width, double value,
+                                  double bias, int threads);
+
+int sdnn_net_n_layers(const sdnn_net *net, int64_t *n);
+/* Device bytes held by the weights (for the roofline byte model). */
+int sdnn_net_weight_bytes(const sdnn_net *net, int64_t *bytes);
+
+/* Stage Y0 (FeatureBatch, CSR) on the device.  Untimed input placement. */
+int sdnn_batch_upload(sdnn_net *net, int64_t n_rows, const int64_t *y_off,
+                      const int64_t *y_cols, const double *y_vals, sdnn_batch **out);
+void sdnn_batch_free(sdnn_batch *batch);
+
+/* Run layers [first_layer, first_layer + n_layers) over a staged batch and
+ * build the category list (the reference's timed region,
+ * engine.py:336-339).  n_layers < 0 means all remaining layers. */
+int sdnn_run(sdnn_net *net, const sdnn_batch *batch, double ymax, int64_t first_layer,
+             int64_t n_layers, sdnn_result **out);
+
+/* sdnn_run that also materialises the final Y for sdnn_result_y_csr. */
+int sdnn_run_y(sdnn_net *net, const sdnn_batch *batch, double ymax, int64_t first_layer,
+               int64_t n_layers, sdnn_result **out);
+
+/* engine.infer end to end: host CSR in, result (with Y) out. */
+int sdnn_infer(sdnn_net *net, int64_t n_rows, const int64_t *y_off, const int64_t *y_cols,
+               const double *y_vals, double ymax, sdnn_result **out);
+
+/* Category list: 1-based rows of the final Y holding any entry, ascending. */
+int sdnn_result_n_categories(const sdnn_result *r, int64_t *n);
+int sdnn_result_categories(const sdnn_result *r, int64_t *buf);
+/* Device time of the layer loop (CUDA events) and host wall time of the
+ * whole call, milliseconds. */
+double sdnn_result_device_ms(const sdnn_result *r);
+double sdnn_result_wall_ms(const sdnn_result *r);
+/* live_rows[l] = rows with an entry entering layer l (l = 0..n_layers),
+ * live_rows[n_layers] = rows alive at the end. */
+int sdnn_result_n_layers(const sdnn_result *r, int64_t *n);
+int sdnn_result_live_rows(const sdnn_result *r, int64_t *live_rows);
+/* Profiling pass: record a CUDA event around every layer launch of later
+ * runs on this handle (off by default; adds one event per layer). */
+int sdnn_net_set_layer_timing(sdnn_net *net, int on);
+/* Per-layer device milliseconds of a run made with layer timing on. */
+int sdnn_result_layer_ms(const sdnn_result *r, double *ms);
+/* Kernel launches the run issued (evidence for bench gpu_launches). */
+int sdnn_result_launches(const sdnn_result *r, int64_t *n);
+/* Final Y as canonical CSR (ascending columns, no zeros) widened to
+ * float64: query nnz first, then fill caller buffers. */
+int sdnn_result_y_nnz(sdnn_result *r, int64_t *nnz);
+int sdnn_result_y_csr(sdnn_result *r, int64_t *off, int64_t *cols, double *vals);
+void sdnn_result_free(sdnn_result *r);
+
+/* engine.spmm: Z = Y * W (n_rows x n_inner times n_inner x n_out), exact
+ * zeros dropped, no epilogue.  Result Y is Z. */
+int sdnn_spmm(int device, int dtype, int64_t n_rows, int64_t n_inner, int64_t n_out,
+              const int64_t *y_off, const int64_t *y_cols, const double *y_vals,
+              const int64_t *w_off, const int64_t *w_cols, const double *w_vals,
+              sdnn_result **out);
+
+/* engine.apply_bias_relu_clamp on a CSR matrix. */
+int sdnn_bias_relu_clamp(int device, int dtype, int64_t n_rows, int64_t n_cols,
+                         const int64_t *off, const int64_t *cols, const double *vals,
+                         double bias, double ymax, sdnn_result **out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

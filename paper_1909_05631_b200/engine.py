@@ -1,0 +1,491 @@
+"""Drop-in for ``sdnnbench.engine`` (reference engine.py:1-340) on B200.
+
+Same entry points, argument meaning and error behaviour as the reference:
+
+* ``infer(model, y0, cfg)``          engine.py:300-324
+* ``infer_timed(model, y0, cfg)``    engine.py:327-340
+* ``spmm(y, w)``                     engine.py:163-175
+* ``apply_bias_relu_clamp(z, b, m)`` engine.py:178-184
+* ``warmup()``                       engine.py:144-155
+* ``InferenceConfig``                engine.py:41-61 (+ ``dtype``, ``devices``)
+
+All arithmetic runs in libsdnn.so (hand-written sm_100a CUDA) through the C
+ABI of include/sdnn.h.  There is no CPU path: without the library or a CUDA
+device every call raises CapacityError.
+
+Modes map onto GPUs the way the reference maps them onto threads:
+``serial`` uses one GPU; ``data_parallel`` splits the batch into contiguous
+row blocks, one per GPU (up to ``workers``), each GPU holding a full weight
+replica, one host thread per GPU (engine.py:237-251); ``pipeline`` runs
+contiguous layer ranges one after another (engine.py:254-297).  Every mode
+produces bit-identical output, as in the reference.
+
+``dtype="f64"`` (default) is bit-exact with the reference; ``dtype="f32"``
+is the throughput path (same algorithm in float arithmetic).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import sys
+import threading
+import time
+import weakref
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import CapacityError, ParameterError, ShapeError
+from .model import CategorySet, FeatureBatch, SparseMatrix
+
+__all__ = [
+    "InferenceConfig",
+    "DEFAULT_YMAX",
+    "DeviceNetwork",
+    "RunResult",
+    "spmm",
+    "apply_bias_relu_clamp",
+    "infer",
+    "infer_timed",
+    "warmup",
+]
+
+DEFAULT_YMAX = 32.0
+MODES = ("serial", "data_parallel", "pipeline")
+DTYPES = {"f32": 0, "f64": 1}
+
+
+@dataclass(frozen=True)
+class InferenceConfig:
+    """Execution knobs; the numeric result never depends on them (for a
+    given dtype)."""
+
+    ymax: float = DEFAULT_YMAX
+    mode: str = "serial"
+    workers: int = 1
+    pipeline_stages: int | None = None
+    batch_tile: int | None = None
+    dtype: str = "f64"
+    devices: tuple | None = None
+
+    def __post_init__(self):
+        if not self.ymax > 0:
+            raise ParameterError(f"ymax must be positive, got {self.ymax}")
+        if self.mode not in MODES:
+            raise ParameterError(f"mode {self.mode!r} is not one of {MODES}")
+        if self.workers < 1:
+            raise ParameterError(f"workers must be >= 1, got {self.workers}")
+        if self.pipeline_stages is not None and self.pipeline_stages < 1:
+            raise ParameterError("pipeline_stages must be >= 1")
+        if self.batch_tile is not None and self.batch_tile < 1:
+            raise ParameterError("batch_tile must be >= 1")
+        if self.dtype not in DTYPES:
+            raise ParameterError(f"dtype {self.dtype!r} is not one of {tuple(DTYPES)}")
+
+
+# ------------------------------------------------------------------ helpers
+
+def _csr(m):
+    """(n_rows, n_cols, off, cols, vals) of any CSR-shaped object."""
+    m = getattr(m, "data", m)
+    off = np.ascontiguousarray(m.row_offsets, dtype=np.int64)
+    cols = np.ascontiguousarray(m.col_indices, dtype=np.int64)
+    vals = np.ascontiguousarray(m.values, dtype=np.float64)
+    return int(m.n_rows), int(m.n_cols), off, cols, vals
+
+
+def _nonempty(a, dtype):
+    return a if a.size else np.zeros(1, dtype)
+
+
+def _family(obj):
+    """Classes (SparseMatrix, FeatureBatch, CategorySet) of the caller's
+    data model, so results come back in kind."""
+    mod = sys.modules.get(type(obj).__module__)
+    fb = type(obj) if hasattr(obj, "data") else getattr(mod, "FeatureBatch", FeatureBatch)
+    data = getattr(obj, "data", obj)
+    sm = type(data) if hasattr(data, "row_offsets") else SparseMatrix
+    cs = getattr(mod, "CategorySet", CategorySet)
+    return sm, fb, cs
+
+
+def _make_matrix(sm_cls, n_rows, n_cols, off, cols, vals):
+    try:
+        return sm_cls(n_rows, n_cols, off, cols, vals, check=False)
+    except TypeError:
+        return sm_cls(n_rows, n_cols, off, cols, vals)
+
+
+_warm_lock = threading.Lock()
+_warm = False
+
+
+def warmup() -> None:
+    """Load libsdnn.so and confirm a CUDA device (engine.py:144-155 forces
+    JIT compilation; here the kernels are precompiled for sm_100a)."""
+    global _warm
+    with _warm_lock:
+        if _warm:
+            return
+        _lib.lib()
+        if _lib.device_count() < 1:
+            raise CapacityError("no CUDA device visible: the B200 engine has no CPU path")
+        _warm = True
+
+
+# ----------------------------------------------------------- device objects
+
+@dataclass
+class RunResult:
+    """Outputs of one device run."""
+
+    categories: np.ndarray      # 1-based, ascending
+    live_rows: np.ndarray       # R_l entering each layer, plus survivors
+    device_ms: float
+    wall_ms: float
+    launches: int
+    y: tuple | None = None      # (off, cols, vals) float64 CSR, when requested
+    layer_ms: np.ndarray | None = None  # per layer, when layer timing is on
+
+
+class DeviceBatch:
+    """Y0 staged in HBM (device CSR)."""
+
+    def __init__(self, net: "DeviceNetwork", n_rows, off, cols, vals):
+        self.net = net
+        self.n_rows = int(n_rows)
+        self.handle = ctypes.c_void_p()
+        _lib.check(_lib.lib().sdnn_batch_upload(
+            net.handle, self.n_rows, _lib.ptr(_nonempty(off, np.int64)),
+            _lib.ptr(_nonempty(cols, np.int64)), _lib.ptr(_nonempty(vals, np.float64)),
+            ctypes.byref(self.handle)))
+
+    def close(self):
+        if self.handle:
+            _lib.lib().sdnn_batch_free(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+class DeviceNetwork:
+    """A network resident on one GPU: every layer converted once to the
+    device ELL layout (untimed, like model loading, engine.py:329-332)."""
+
+    def __init__(self, n_neurons: int, device: int = 0, dtype: str = "f32"):
+        warmup()
+        if dtype not in DTYPES:
+            raise ParameterError(f"dtype {dtype!r} is not one of {tuple(DTYPES)}")
+        self.n = int(n_neurons)
+        self.device = int(device)
+        self.dtype = dtype
+        self.handle = ctypes.c_void_p()
+        _lib.check(_lib.lib().sdnn_net_create(self.device, DTYPES[dtype], self.n,
+                                              ctypes.byref(self.handle)))
+        self.n_layers = 0
+        self.lock = threading.Lock()  # one handle, one host thread at a time
+
+    @classmethod
+    def from_model(cls, model, device: int = 0, dtype: str = "f32") -> "DeviceNetwork":
+        net = cls(model.neurons_per_layer, device, dtype)
+        for lw in model.layers:
+            net.add_layer_csr(lw.weights, lw.bias)
+        return net
+
+    def add_layer_csr(self, w, bias: float) -> None:
+        n_rows, n_cols, off, cols, vals = _csr(w)
+        if (n_rows, n_cols) != (self.n, self.n):
+            raise ShapeError(f"layer is {n_rows}x{n_cols}, network has {self.n} neurons")
+        _lib.check(_lib.lib().sdnn_net_add_layer_csr(
+            self.handle, _lib.ptr(off), _lib.ptr(_nonempty(cols, np.int64)),
+            _lib.ptr(_nonempty(vals, np.float64)), int(off[-1]), float(bias)))
+        self.n_layers += 1
+
+    def add_layer_ell(self, idx: np.ndarray, vals: np.ndarray | None, bias: float) -> None:
+        idx = np.ascontiguousarray(idx, dtype=np.int32)
+        width = idx.shape[1] if idx.ndim == 2 else 0
+        v = None if vals is None else np.ascontiguousarray(vals, dtype=np.float64)
+        _lib.check(_lib.lib().sdnn_net_add_layer_ell(self.handle, width, _lib.ptr(idx),
+                                                     _lib.ptr(v), float(bias)))
+        self.n_layers += 1
+
+    def add_permunion_layers(self, seed: int, first_layer: int, count: int, width: int,
+                             value: float, bias: float, threads: int = 0) -> None:
+        _lib.check(_lib.lib().sdnn_net_add_layers_permunion(
+            self.handle, int(seed), int(first_layer), int(count), int(width), float(value),
+            float(bias), int(threads)))
+        self.n_layers += int(count)
+
+    def set_layer_timing(self, on: bool) -> None:
+        _lib.check(_lib.lib().sdnn_net_set_layer_timing(self.handle, 1 if on else 0))
+
+    def weight_bytes(self) -> int:
+        b = ctypes.c_int64()
+        _lib.check(_lib.lib().sdnn_net_weight_bytes(self.handle, ctypes.byref(b)))
+        return b.value
+
+    def upload(self, y0) -> DeviceBatch:
+        n_rows, n_cols, off, cols, vals = _csr(y0)
+        if n_cols != self.n:
+            raise ShapeError(f"input has {n_cols} columns but the model expects {self.n} neurons")
+        return DeviceBatch(self, n_rows, off, cols, vals)
+
+    def upload_csr(self, n_rows, off, cols, vals) -> DeviceBatch:
+        return DeviceBatch(self, n_rows, np.ascontiguousarray(off, np.int64),
+                           np.ascontiguousarray(cols, np.int64), np.ascontiguousarray(vals, np.float64))
+
+    def run(self, batch: DeviceBatch, ymax: float = DEFAULT_YMAX, first_layer: int = 0,
+            n_layers: int = -1, want_y: bool = False) -> RunResult:
+        L = _lib.lib()
+        h = ctypes.c_void_p()
+        fn = L.sdnn_run_y if want_y else L.sdnn_run
+        _lib.check(fn(self.handle, batch.handle, float(ymax), int(first_layer), int(n_layers),
+                      ctypes.byref(h)))
+        try:
+            return _collect(h, batch.n_rows, want_y)
+        finally:
+            L.sdnn_result_free(h)
+
+    def infer_host(self, y0, ymax: float = DEFAULT_YMAX) -> RunResult:
+        """End-to-end C-ABI call (sdnn_infer): host CSR in, categories + Y out."""
+        n_rows, n_cols, off, cols, vals = _csr(y0)
+        if n_cols != self.n:
+            raise ShapeError(f"input has {n_cols} columns but the model expects {self.n} neurons")
+        L = _lib.lib()
+        h = ctypes.c_void_p()
+        _lib.check(L.sdnn_infer(self.handle, n_rows, _lib.ptr(_nonempty(off, np.int64)),
+                                _lib.ptr(_nonempty(cols, np.int64)),
+                                _lib.ptr(_nonempty(vals, np.float64)), float(ymax), ctypes.byref(h)))
+        try:
+            return _collect(h, n_rows, True)
+        finally:
+            L.sdnn_result_free(h)
+
+    def close(self):
+        if self.handle:
+            _lib.lib().sdnn_net_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+def _collect(h, n_rows: int, want_y: bool) -> RunResult:
+    L = _lib.lib()
+    n = ctypes.c_int64()
+    _lib.check(L.sdnn_result_n_categories(h, ctypes.byref(n)))
+    cats = np.zeros(max(n.value, 1), np.int64)
+    _lib.check(L.sdnn_result_categories(h, _lib.ptr(cats)))
+    cats = cats[:n.value]
+    nl = ctypes.c_int64()
+    _lib.check(L.sdnn_result_n_layers(h, ctypes.byref(nl)))
+    live = np.zeros(nl.value + 1, np.int64)
+    _lib.check(L.sdnn_result_live_rows(h, _lib.ptr(live)))
+    launches = ctypes.c_int64()
+    _lib.check(L.sdnn_result_launches(h, ctypes.byref(launches)))
+    layer_ms = np.zeros(max(nl.value, 1))
+    if L.sdnn_result_layer_ms(h, _lib.ptr(layer_ms)) == 0:
+        layer_ms = layer_ms[:nl.value]
+    else:
+        layer_ms = None
+    y = None
+    if want_y:
+        nnz = ctypes.c_int64()
+        _lib.check(L.sdnn_result_y_nnz(h, ctypes.byref(nnz)))
+        off = np.zeros(n_rows + 1, np.int64)
+        cols = np.zeros(max(nnz.value, 1), np.int64)
+        vals = np.zeros(max(nnz.value, 1), np.float64)
+        _lib.check(L.sdnn_result_y_csr(h, _lib.ptr(off), _lib.ptr(cols), _lib.ptr(vals)))
+        y = (off, cols[:nnz.value], vals[:nnz.value])
+    return RunResult(cats, live, L.sdnn_result_device_ms(h), L.sdnn_result_wall_ms(h),
+                     launches.value, y, layer_ms)
+
+
+# ------------------------------------------------------- network residency
+
+_cache_lock = threading.Lock()
+_cache: dict = {}
+
+
+def _device_network(model, device: int, dtype: str) -> DeviceNetwork:
+    """Weights are uploaded once per (model object, device, dtype)."""
+    key = id(model)
+    with _cache_lock:
+        entry = _cache.get(key)
+        if entry is None or entry[0]() is not model:
+            try:
+                ref = weakref.ref(model, lambda _r, k=key: _cache.pop(k, None))
+            except TypeError:
+                ref = lambda m=model: m  # noqa: E731 -- unweakrefable: keep alive
+            entry = (ref, {})
+            _cache[key] = entry
+        nets = entry[1]
+        net = nets.get((device, dtype))
+    if net is None:
+        net = DeviceNetwork.from_model(model, device, dtype)
+        with _cache_lock:
+            nets[(device, dtype)] = net
+    return net
+
+
+def _devices(cfg: InferenceConfig) -> list[int]:
+    avail = _lib.device_count()
+    if cfg.devices is not None:
+        devs = [int(d) for d in cfg.devices]
+        if any(d < 0 or d >= avail for d in devs):
+            raise ParameterError(f"devices {devs} not all visible ({avail} present)")
+        return devs
+    if cfg.mode == "data_parallel":
+        return list(range(max(1, min(cfg.workers, avail))))
+    return [0]
+
+
+def _stage_partition(n_layers: int, n_stages: int) -> list[tuple[int, int]]:
+    """Contiguous near-equal layer ranges (engine.py:226-229)."""
+    bounds = np.linspace(0, n_layers, n_stages + 1).astype(int)
+    return [(int(bounds[i]), int(bounds[i + 1])) for i in range(n_stages)]
+
+
+def _run_block(model, dtype, device, ymax, n_rows, off, cols, vals, ranges):
+    """Push one row block through the given layer ranges on one GPU."""
+    net = _device_network(model, device, dtype)
+    with net.lock:
+        for lo, hi in ranges:
+            batch = net.upload_csr(n_rows, off, cols, vals)
+            try:
+                res = net.run(batch, ymax, lo, hi - lo, want_y=True)
+            finally:
+                batch.close()
+            off, cols, vals = res.y
+    return off, cols, vals
+
+
+def infer(model, y0, cfg: InferenceConfig | None = None):
+    """Run every layer of the model over the batch on the GPU(s); output is
+    bit-identical across modes and device counts (engine.py:300-324)."""
+    cfg = cfg or InferenceConfig()
+    if y0.n_neurons != model.neurons_per_layer:
+        raise ShapeError(
+            f"input has {y0.n_neurons} columns but the model expects "
+            f"{model.neurons_per_layer} neurons"
+        )
+    if cfg.pipeline_stages is not None and cfg.pipeline_stages > model.n_layers:
+        raise ParameterError(
+            f"{cfg.pipeline_stages} pipeline stages cannot partition {model.n_layers} layers"
+        )
+    warmup()
+    sm_cls, fb_cls, _ = _family(y0)
+    n_rows, n_cols, off, cols, vals = _csr(y0)
+    L = model.n_layers
+    if cfg.mode == "pipeline":
+        stages = cfg.pipeline_stages or max(1, min(cfg.workers, L))
+        ranges = _stage_partition(L, min(stages, L))
+    else:
+        ranges = [(0, L)]
+    devs = _devices(cfg)
+    if len(devs) == 1 or n_rows <= 1:
+        o, c, v = _run_block(model, cfg.dtype, devs[0], cfg.ymax, n_rows, off, cols, vals, ranges)
+    else:
+        per = -(-n_rows // len(devs))
+        spans = [(s, min(s + per, n_rows)) for s in range(0, n_rows, per)]
+
+        def work(i):
+            lo, hi = spans[i]
+            base = off[lo]
+            return _run_block(model, cfg.dtype, devs[i], cfg.ymax, hi - lo, off[lo:hi + 1] - base,
+                              cols[base:off[hi]], vals[base:off[hi]], ranges)
+
+        with ThreadPoolExecutor(max_workers=len(spans)) as pool:
+            blocks = list(pool.map(work, range(len(spans))))
+        o = np.zeros(n_rows + 1, np.int64)
+        pos, base = 0, 0
+        for (bo, _, _) in blocks:
+            r = bo.size - 1
+            o[pos + 1:pos + r + 1] = bo[1:] + base
+            base += int(bo[-1])
+            pos += r
+        c = np.concatenate([b[1] for b in blocks])
+        v = np.concatenate([b[2] for b in blocks])
+    return fb_cls(_make_matrix(sm_cls, n_rows, model.neurons_per_layer, o, c, v))
+
+
+def categorize(final):
+    """challenge.categorize (challenge.py:60-67)."""
+    _, _, cs_cls = _family(final)
+    counts = np.diff(np.asarray(final.data.row_offsets))
+    return cs_cls((np.nonzero(counts > 0)[0] + 1).tolist())
+
+
+def infer_timed(model, y0, cfg: InferenceConfig | None = None):
+    """Timed challenge region, inference plus categorization
+    (engine.py:327-340).  Weight upload happens before the clock, like the
+    reference's model loading."""
+    cfg = cfg or InferenceConfig()
+    warmup()
+    for d in _devices(cfg):
+        _device_network(model, d, cfg.dtype)
+    start = time.perf_counter()
+    result = infer(model, y0, cfg)
+    categories = categorize(result)
+    elapsed = time.perf_counter() - start
+    return result, categories, elapsed
+
+
+def spmm(y, w, dtype: str = "f64", device: int = 0):
+    """Z = Y * W with ascending-index accumulation, exact zeros dropped
+    (engine.py:163-175)."""
+    data = getattr(y, "data", y)
+    if data.n_cols != w.n_rows:
+        raise ShapeError(f"cannot multiply {(data.n_rows, data.n_cols)} by {(w.n_rows, w.n_cols)}: "
+                         "inner extents differ")
+    if dtype not in DTYPES:
+        raise ParameterError(f"dtype {dtype!r} is not one of {tuple(DTYPES)}")
+    warmup()
+    sm_cls = type(w) if hasattr(w, "row_offsets") else SparseMatrix
+    yr, yc, yo, ycols, yvals = _csr(data)
+    wr, wc, wo, wcols, wvals = _csr(w)
+    L = _lib.lib()
+    h = ctypes.c_void_p()
+    _lib.check(L.sdnn_spmm(device, DTYPES[dtype], yr, wr, wc, _lib.ptr(_nonempty(yo, np.int64)),
+                           _lib.ptr(_nonempty(ycols, np.int64)), _lib.ptr(_nonempty(yvals, np.float64)),
+                           _lib.ptr(wo), _lib.ptr(_nonempty(wcols, np.int64)),
+                           _lib.ptr(_nonempty(wvals, np.float64)), ctypes.byref(h)))
+    try:
+        res = _collect(h, yr, True)
+    finally:
+        L.sdnn_result_free(h)
+    o, c, v = res.y
+    return _make_matrix(sm_cls, yr, wc, o, c, v)
+
+
+def apply_bias_relu_clamp(z, bias: float, ymax: float = DEFAULT_YMAX, dtype: str = "f64",
+                          device: int = 0):
+    """Bias stored entries only, rectify, clamp (engine.py:178-184)."""
+    if dtype not in DTYPES:
+        raise ParameterError(f"dtype {dtype!r} is not one of {tuple(DTYPES)}")
+    warmup()
+    sm_cls = type(z) if hasattr(z, "row_offsets") else SparseMatrix
+    n_rows, n_cols, off, cols, vals = _csr(z)
+    L = _lib.lib()
+    h = ctypes.c_void_p()
+    _lib.check(L.sdnn_bias_relu_clamp(device, DTYPES[dtype], n_rows, max(n_cols, 1),
+                                      _lib.ptr(_nonempty(off, np.int64)),
+                                      _lib.ptr(_nonempty(cols, np.int64)),
+                                      _lib.ptr(_nonempty(vals, np.float64)), float(bias), float(ymax),
+                                      ctypes.byref(h)))
+    try:
+        res = _collect(h, n_rows, True)
+    finally:
+        L.sdnn_result_free(h)
+    o, c, v = res.y
+    return _make_matrix(sm_cls, n_rows, n_cols, o, c, v)

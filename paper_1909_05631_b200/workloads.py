@@ -1,0 +1,103 @@
+"""BASELINE.json workloads (configs[0..4]) and the live companions.
+
+Synthetic stand-ins, generated from seeds: the paper's inputs are MNIST-
+derived images on RadiX-Net networks, neither of which is
+available here.  W_l is the union of 32 seeded permutation matrices (exactly
+32 nonzeros per row and column, each `value`), Y0 rows are side x side
+binary images with Bernoulli(p) pixels in the centred square.
+
+C1..C5 as specified die by layer 2-3, so K2 (the C4/C5
+generator with weight 0.125 = 2^-3) is carried beside them as the live-row
+throughput companion: survivors saturate at YMAX and stay dense.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from . import _lib
+
+WEIGHT_SEED = 20190912
+IMAGE_SEED = 1909
+
+
+@dataclass(frozen=True)
+class Workload:
+    name: str
+    n: int
+    layers: int
+    batch: int
+    side: int
+    square: int
+    p: float
+    bias: float
+    width: int = 32
+    value: float = 0.0625
+    ymax: float = 32.0
+    weight_seed: int = WEIGHT_SEED
+    image_seed: int = IMAGE_SEED
+
+    @property
+    def edges(self) -> int:
+        """Nominal edges (inputs x connections), the challenge rate numerator."""
+        return self.batch * self.n * self.width * self.layers
+
+    def with_(self, **kw) -> "Workload":
+        return replace(self, **kw)
+
+
+CONFIGS = {
+    "C1": Workload("C1", 1024, 120, 60000, 32, 20, 0.35, -0.30),
+    "C2": Workload("C2", 4096, 480, 60000, 64, 40, 0.35, -0.35),
+    "C3": Workload("C3", 16384, 1920, 60000, 128, 80, 0.35, -0.40),
+    "C4": Workload("C4", 65536, 1920, 60000, 256, 160, 0.35, -0.45),
+    "C5": Workload("C5", 65536, 120, 60000, 256, 160, 0.35, -0.45),
+    "K2": Workload("K2", 65536, 1920, 60000, 256, 160, 0.35, -0.45, value=0.125),
+}
+C5_SWEEP = [(b, p) for b in (1000, 15000, 60000, 240000) for p in (0.1, 0.35, 0.7)]
+
+
+def _threads() -> int:
+    return max(1, min(os.cpu_count() or 1, 64))
+
+
+def images(w: Workload, n_rows: int | None = None, threads: int | None = None, row0: int = 0):
+    """Rows [row0, row0 + n_rows) of Y0 as CSR arrays (off int64, cols
+    int64, vals float64); n_rows defaults to the whole batch."""
+    g = _lib.gen()
+    B = w.batch - row0 if n_rows is None else int(n_rows)
+    t = threads or _threads()
+    cnt = np.zeros(max(B, 1), np.int64)
+    _lib.check_gen(g.sdnn_gen_images_count(w.image_seed, row0, B, w.side, w.square, w.p, t,
+                                           _lib.ptr(cnt)))
+    off = np.zeros(B + 1, np.int64)
+    np.cumsum(cnt[:B], out=off[1:])
+    nnz = int(off[-1])
+    cols = np.zeros(max(nnz, 1), np.int64)
+    vals = np.zeros(max(nnz, 1), np.float64)
+    _lib.check_gen(g.sdnn_gen_images_fill(w.image_seed, row0, B, w.side, w.square, w.p, t,
+                                          _lib.ptr(off), _lib.ptr(cols), None, _lib.ptr(vals)))
+    return off, cols[:nnz], vals[:nnz]
+
+
+def layer_ell(w: Workload, layer: int) -> np.ndarray:
+    """Layer `layer` as ELL by output column, [n][width] int32 ascending."""
+    idx = np.zeros((w.n, w.width), np.int32)
+    _lib.check_gen(_lib.gen().sdnn_gen_permunion_ell(w.weight_seed, layer, w.n, w.width, _lib.ptr(idx)))
+    return idx
+
+
+def layer_csr(w: Workload, layer: int):
+    """Layer `layer` in the reference's CSR-by-input layout (off, cols, vals)."""
+    idx = layer_ell(w, layer)
+    vals = np.full(idx.size, w.value, np.float64)
+    off = np.zeros(w.n + 1, np.int64)
+    cols = np.zeros(idx.size, np.int64)
+    out = np.zeros(idx.size, np.float64)
+    _lib.check_gen(_lib.gen().sdnn_gen_ell_to_csr(w.n, w.n, w.width, _lib.ptr(idx), _lib.ptr(vals),
+                                                  _lib.ptr(off), _lib.ptr(cols), _lib.ptr(out)))
+    return off, cols, out

@@ -1,0 +1,289 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle.
+
+float64 must equal the reference bit for bit (golden vectors produced by
+the reference itself, tests/golden) and the oracle's float64 instance.
+float32 must equal the oracle's float32 instance bit for bit (same
+algorithm, same order), and the category list must match the float64
+reference wherever float32 keeps categories (the BASELINE configs); on the
+fp32-hostile RadiX-Net workload the float32 tolerance is reported, not
+asserted bitwise.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+import goldens
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1909_05631_b200 import engine as E  # noqa: E402
+from paper_1909_05631_b200 import workloads as W  # noqa: E402
+from paper_1909_05631_b200.errors import ParameterError, ShapeError  # noqa: E402
+from paper_1909_05631_b200.model import (  # noqa: E402
+    FeatureBatch,
+    LayerWeights,
+    NetworkModel,
+    SparseMatrix,
+)
+
+
+def sm(c: O.CSR) -> SparseMatrix:
+    return SparseMatrix(c.n_rows, c.n_cols, c.off, c.cols, c.vals, check=False)
+
+
+def model_of(layers, bias, n):
+    return NetworkModel(n, tuple(LayerWeights(sm(w), float(b)) for w, b in zip(layers, bias)))
+
+
+def as_csr(fb) -> O.CSR:
+    d = fb.data
+    return O.CSR(d.n_rows, d.n_cols, np.asarray(d.row_offsets), np.asarray(d.col_indices),
+                 np.asarray(d.values))
+
+
+@pytest.fixture
+def env():
+    saved = dict(os.environ)
+    yield os.environ
+    os.environ.clear()
+    os.environ.update(saved)
+
+
+# ------------------------------------------------------------ golden vectors
+
+def test_general_goldens_f64_bit_exact():
+    for i, t in enumerate(goldens.general()):
+        model = model_of(t["layers"], t["bias"], t["n"])
+        out = E.infer(model, FeatureBatch(sm(t["y0"])))
+        assert as_csr(out).identical(t["y"]), f"instance {i}"
+        assert np.array_equal(np.asarray(E.categorize(out).image_rows), t["cats"])
+
+
+@pytest.mark.parametrize("cfg", [
+    dict(mode="data_parallel", workers=2, devices=(0, 0)),
+    dict(mode="data_parallel", workers=3, devices=(0, 0, 0)),
+    dict(mode="pipeline", pipeline_stages=2),
+    dict(mode="pipeline", workers=8),
+])
+def test_modes_bit_identical(cfg):
+    for t in goldens.general()[:12]:
+        model = model_of(t["layers"], t["bias"], t["n"])
+        layers = len(t["layers"])
+        c = dict(cfg)
+        if c.get("pipeline_stages", 0) > layers:
+            c["pipeline_stages"] = layers
+        out = E.infer(model, FeatureBatch(sm(t["y0"])), E.InferenceConfig(**c))
+        assert as_csr(out).identical(t["y"])
+
+
+def test_general_goldens_f32_is_the_oracle_float_instance():
+    for t in goldens.general():
+        model = model_of(t["layers"], t["bias"], t["n"])
+        out = E.infer(model, FeatureBatch(sm(t["y0"])), E.InferenceConfig(dtype="f32"))
+        want = O.infer(t["layers"], t["bias"], t["y0"], precision=32)
+        assert as_csr(out).identical(want)
+
+
+def test_radixnet_digits_f64_bit_exact_and_f32_tolerance():
+    r = goldens.radixnet()
+    for L, y, cats in ((24, r["y24"], r["cats24"]), (120, r["y120"], r["cats120"])):
+        model = model_of(r["layers"][:L], r["bias"][:L], r["n"])
+        out = E.infer(model, FeatureBatch(sm(r["y0"])))
+        assert as_csr(out).identical(y)
+        out32 = E.infer(model, FeatureBatch(sm(r["y0"])), E.InferenceConfig(dtype="f32"))
+        want32 = O.infer(r["layers"][:L], r["bias"][:L], r["y0"], precision=32)
+        assert as_csr(out32).identical(want32)
+        # categories survive float32 on this workload (values saturate or die)
+        assert np.array_equal(O.categorize(as_csr(out32)), cats)
+
+
+# -------------------------------------------------------------- KATs on GPU
+
+def csr(dense):
+    return sm(O.CSR.from_dense(np.asarray(dense, np.float64)))
+
+
+class TestKAT:
+    def test_spmm_identity_and_hand_sum(self):
+        z = E.spmm(FeatureBatch(csr([[1.0, 0.0]])), csr(np.eye(2)))
+        assert np.array_equal(z.to_dense(), [[1.0, 0.0]])
+        z = E.spmm(FeatureBatch(csr([[1.0, 1.0]])), csr([[.5, .5], [.5, .5]]))
+        assert np.array_equal(z.to_dense(), [[1.0, 1.0]])
+
+    def test_spmm_empty_and_rectangular(self):
+        y = SparseMatrix.empty(3, 4)
+        w = csr(np.pad([[2.0]], ((0, 3), (0, 4))))  # 4 x 5
+        z = E.spmm(FeatureBatch(y), w)
+        assert z.shape == (3, 5) and z.nnz == 0
+
+    def test_spmm_shape_mismatch(self):
+        with pytest.raises(ShapeError):
+            E.spmm(FeatureBatch(csr([[1.0, 0.0]])), csr(np.eye(3)))
+
+    def test_exact_zero_dropped(self):
+        z = E.spmm(FeatureBatch(csr([[1.0, 1.0]])), csr([[.5, 0], [-.5, 0]]))
+        assert z.nnz == 0
+
+    def test_ascending_inner_order(self, rng):
+        yd = (rng.random((4, 40)) < 0.8).astype(float)
+        wd = rng.uniform(-1, 1, size=(40, 7))
+        z = E.spmm(FeatureBatch(csr(yd)), csr(wd))
+        want = O.spmm(O.CSR.from_dense(yd), O.CSR.from_dense(wd))
+        assert np.array_equal(z.to_dense(), want.to_dense())
+
+    def test_bias_relu_clamp(self):
+        assert E.apply_bias_relu_clamp(csr([[0.5]]), -0.3).values.tolist() == [0.5 + -0.3]
+        assert E.apply_bias_relu_clamp(csr([[0.2]]), -0.3).nnz == 0
+        assert E.apply_bias_relu_clamp(csr([[0.25]]), -0.25).nnz == 0
+        assert E.apply_bias_relu_clamp(csr([[40.0]]), 0.0, 32.0).values.tolist() == [32.0]
+        out = E.apply_bias_relu_clamp(csr([[0.5, 0.0]]), 0.4)
+        assert out.col_indices.tolist() == [0] and out.values.tolist() == [0.5 + 0.4]
+
+    def test_cancelled_entry_gets_no_bias(self):
+        z = E.spmm(FeatureBatch(csr([[1.0, 1.0]])), csr([[.75, .5], [.25, -.5]]))
+        assert z.col_indices.tolist() == [0]
+        b = E.apply_bias_relu_clamp(z, 0.4)
+        assert b.col_indices.tolist() == [0] and b.values.tolist() == [1.0 + 0.4]
+
+    def test_worked_example_and_clamp(self):
+        model = NetworkModel(2, (LayerWeights(csr([[.5, .5], [0, 1.0]]), -0.3),))
+        out = E.infer(model, FeatureBatch(csr([[1.0, 0.0]])))
+        assert np.array_equal(out.data.to_dense(), [[0.5 + -0.3, 0.5 + -0.3]])
+        model = NetworkModel(1, (LayerWeights(csr([[5.0]]), 0.0),))
+        assert E.infer(model, FeatureBatch(csr([[8.0]]))).data.values.tolist() == [32.0]
+
+    def test_validation(self):
+        model = NetworkModel(2, (LayerWeights(csr(np.eye(2)), 0.0),))
+        with pytest.raises(ShapeError):
+            E.infer(model, FeatureBatch(csr([[1.0, 0.0, 1.0]])))
+        with pytest.raises(ParameterError):
+            E.infer(model, FeatureBatch(csr([[1.0, 0.0]])),
+                    E.InferenceConfig(mode="pipeline", pipeline_stages=5))
+
+    def test_empty_and_single_row_batches(self):
+        t = goldens.general()[0]
+        model = model_of(t["layers"], t["bias"], t["n"])
+        out = E.infer(model, FeatureBatch(SparseMatrix.empty(0, t["n"])))
+        assert out.data.shape == (0, t["n"])
+        out = E.infer(model, FeatureBatch(SparseMatrix.empty(5, t["n"])))
+        assert out.data.nnz == 0 and out.data.n_rows == 5
+        one = O.CSR(1, t["n"], t["y0"].off[:2], t["y0"].cols[:t["y0"].off[1]],
+                    t["y0"].vals[:t["y0"].off[1]])
+        got = as_csr(E.infer(model, FeatureBatch(sm(one))))
+        assert got.identical(O.infer(t["layers"], t["bias"], one))
+
+    def test_infer_timed(self):
+        t = goldens.general()[3]
+        model = model_of(t["layers"], t["bias"], t["n"])
+        out, cats, sec = E.infer_timed(model, FeatureBatch(sm(t["y0"])))
+        assert sec > 0 and as_csr(out).identical(t["y"])
+        assert np.array_equal(np.asarray(cats.image_rows), t["cats"])
+
+
+# ------------------------------------------------- kernel geometry variants
+
+def permunion_case(n, layers, rows, value, p=0.35):
+    side = int(round(n ** 0.5))
+    w = W.Workload("t", n, layers, rows, side, int(side * 0.625), p, -0.45, value=value)
+    off, cols, vals = W.images(w)
+    return w, O.CSR(rows, n, off, cols, vals), [O.CSR(n, n, *W.layer_csr(w, l)) for l in range(layers)]
+
+
+@pytest.mark.parametrize("budget,R", [("2048", "1"), ("8192", "2"), ("65536", "8"), ("4096", "4")])
+@pytest.mark.parametrize("dtype,prec", [("f64", 64), ("f32", 32)])
+def test_chunked_and_grouped_geometry(env, budget, R, dtype, prec):
+    env["SDNN_SMEM_BUDGET"] = budget
+    env["SDNN_R"] = R
+    w, y0, layers = permunion_case(1024, 5, 97, 0.125)
+    net = E.DeviceNetwork(w.n, 0, dtype)
+    for l in range(w.layers):
+        net.add_layer_csr(sm(layers[l]), w.bias)
+    res = net.run(net.upload_csr(y0.n_rows, y0.off, y0.cols, y0.vals), w.ymax, want_y=True)
+    want = O.infer(layers, [w.bias] * w.layers, y0, precision=prec, threads=4)
+    assert O.CSR(y0.n_rows, w.n, *res.y).identical(want)
+    assert res.live_rows[0] == np.count_nonzero(np.diff(y0.off))
+
+
+@pytest.mark.parametrize("n", [4096, 16384, 65536])
+def test_large_n_live_rows_f32_and_f64(n):
+    rows = {4096: 48, 16384: 24, 65536: 8}[n]
+    w, y0, layers = permunion_case(n, 6, rows, 0.125)
+    for dtype, prec in (("f32", 32), ("f64", 64)):
+        net = E.DeviceNetwork(w.n, 0, dtype)
+        net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias)
+        res = net.run(net.upload_csr(y0.n_rows, y0.off, y0.cols, y0.vals), w.ymax, want_y=True)
+        want = O.infer(layers, [w.bias] * w.layers, y0, precision=prec, threads=8)
+        assert O.CSR(y0.n_rows, w.n, *res.y).identical(want), dtype
+        net.close()
+
+
+def test_wave_splitting_does_not_change_bits(env):
+    env["SDNN_WAVE_ROWS"] = "37"
+    w, y0, layers = permunion_case(1024, 4, 200, 0.125)
+    net = E.DeviceNetwork(w.n, 0, "f64")
+    net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias)
+    res = net.run(net.upload_csr(y0.n_rows, y0.off, y0.cols, y0.vals), w.ymax, want_y=True)
+    want = O.infer(layers, [w.bias] * w.layers, y0, threads=4)
+    assert O.CSR(y0.n_rows, w.n, *res.y).identical(want)
+
+
+def test_e2e_host_call_matches_device_resident_run():
+    w, y0, layers = permunion_case(1024, 8, 300, 0.125)
+    net = E.DeviceNetwork(w.n, 0, "f32")
+    net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias)
+    a = net.infer_host(sm(y0))
+    b = net.run(net.upload_csr(y0.n_rows, y0.off, y0.cols, y0.vals), w.ymax, want_y=True)
+    assert np.array_equal(a.categories, b.categories)
+    assert all(np.array_equal(x, y) for x, y in zip(a.y, b.y))
+
+
+# ------------------------------------------------ BASELINE configs, full size
+
+def test_c1_as_specified_full_size():
+    """C1 (N=1024, L=120, 60,000 rows) in full against the oracle; the
+    category list must be bit-exact in both precisions."""
+    w = W.CONFIGS["C1"]
+    off, cols, vals = W.images(w)
+    y0 = O.CSR(w.batch, w.n, off, cols, vals)
+    layers = [O.CSR(w.n, w.n, *W.layer_csr(w, l)) for l in range(w.layers)]
+    want = O.infer(layers, [w.bias] * w.layers, y0, threads=os.cpu_count() or 8)
+    for dtype in ("f32", "f64"):
+        net = E.DeviceNetwork(w.n, 0, dtype)
+        net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias)
+        res = net.run(net.upload_csr(w.batch, off, cols, vals), w.ymax, want_y=True)
+        assert np.array_equal(res.categories, O.categorize(want)), dtype
+        assert O.CSR(w.batch, w.n, *res.y).nnz == want.nnz
+        if dtype == "f64":
+            assert O.CSR(w.batch, w.n, *res.y).identical(want)
+        net.close()
+
+
+def test_c4_shape_full_batch_row_sample_consistency():
+    """Flagship width at full batch: rows are independent, so a 64-row
+    sample run alone (and by the oracle) must agree with the full run."""
+    w = W.CONFIGS["K2"].with_(layers=8)
+    off, cols, vals = W.images(w)
+    net = E.DeviceNetwork(w.n, 0, "f32")
+    net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias)
+    full = net.run(net.upload_csr(w.batch, off, cols, vals), w.ymax)
+    assert full.live_rows[0] == w.batch
+    rng = np.random.default_rng(3)
+    sample = np.sort(rng.choice(w.batch, 64, replace=False))
+    s_off = np.zeros(65, np.int64)
+    np.cumsum(np.diff(off)[sample], out=s_off[1:])
+    s_cols = np.concatenate([cols[off[r]:off[r + 1]] for r in sample])
+    s_vals = np.concatenate([vals[off[r]:off[r + 1]] for r in sample])
+    part = net.run(net.upload_csr(64, s_off, s_cols, s_vals), w.ymax, want_y=True)
+    in_full = np.isin(sample + 1, full.categories)
+    assert np.array_equal(np.nonzero(in_full)[0] + 1, part.categories)
+    layers = [O.CSR(w.n, w.n, *W.layer_csr(w, l)) for l in range(w.layers)]
+    want = O.infer(layers, [w.bias] * w.layers, O.CSR(64, w.n, s_off, s_cols, s_vals),
+                   precision=32, threads=os.cpu_count() or 8)
+    assert O.CSR(64, w.n, *part.y).identical(want)
