@@ -23,6 +23,9 @@
 #include "../../include/sdnn.h"
 #include "sdnn_kernels.cuh"
 
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
 using namespace sdnn;
 
 namespace {
@@ -81,10 +84,10 @@ void parallel_for(int64_t n, F f) {
 }
 
 struct DevLayer {
-    int width = 0;
-    int32_t* idx = nullptr;  // [width][n]
-    void* val = nullptr;     // [width][n] of T
-    uint16_t* bnd = nullptr; // [(n_chunks+1)][n] when chunked
+    int width = 0;           // real slots (max column degree)
+    int wp = 0;              // padded to a multiple of 32
+    int32_t* idx = nullptr;  // [n][wp], -1 = padding
+    void* val = nullptr;     // [n][wp] of T
     double bias = 0;
     int64_t bytes = 0;
 };
@@ -96,30 +99,38 @@ struct sdnn_net {
     int dtype = SDNN_F32;
     int64_t n = 0;
     int elem = 4;
-    // launch geometry of the layer kernel for this (n, dtype)
-    int R = 1, n_chunks = 1, chunk_len = 0, threads = 256, blocks = 0;
-    size_t smem = 0;
     int sm_count = 0;
+    int jb = 512;  // outputs per work item
     std::vector<DevLayer> layers;
+    void* descs = nullptr;  // device LayerDesc<T>[layers]
+    int64_t descs_n = 0;    // layers mirrored in `descs`
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // run scratch, grown on demand
-    void* ybuf[2] = {nullptr, nullptr};
-    int64_t ycap = 0;  // rows per buffer
-    int32_t* rows[2] = {nullptr, nullptr};
+    void* slab[2] = {nullptr, nullptr};
+    uint8_t* mask[2] = {nullptr, nullptr};
+    int64_t tcap = 0;  // tiles per buffer
+    int32_t* rowid = nullptr;
+    int32_t* rowlist = nullptr;
     int64_t rcap = 0;
-    int32_t* counts = nullptr;
+    uint32_t* alive = nullptr;
+    int64_t acap = 0;
+    int32_t* tile_count = nullptr;
+    int64_t* live_rows = nullptr;
+    unsigned long long* stamps = nullptr;
+    unsigned* bar = nullptr;
+    int32_t* n_sel = nullptr;
     int64_t ccap = 0;
+    void* cub_tmp = nullptr;
+    size_t cub_cap = 0;
     void* pinned = nullptr;
     size_t pinned_cap = 0;
-    // optional per-layer events (profiling pass, off in timed runs)
     int layer_timing = 0;
-    std::vector<cudaEvent_t> lev;
 };
 
 struct sdnn_batch {
     sdnn_net* net = nullptr;
-    int64_t n_rows = 0, nnz = 0;
+    int64_t n_rows = 0, nnz = 0, n_cols = 0;
     int64_t* off = nullptr;
     int32_t* cols = nullptr;
     void* vals = nullptr;
@@ -145,232 +156,107 @@ int set_device(const sdnn_net* net) {
     return SDNN_OK;
 }
 
-template <typename T>
-const void* layer_fn(int R) {
-    switch (R) {
-        case 1: return (const void*)layer_kernel<T, 1>;
-        case 2: return (const void*)layer_kernel<T, 2>;
-        case 4: return (const void*)layer_kernel<T, 4>;
-        default: return (const void*)layer_kernel<T, 8>;
-    }
-}
+int64_t round16(int64_t x) { return (x + 15) / 16 * 16; }
 
-const void* layer_fn_for(const sdnn_net* net) {
-    return net->dtype == SDNN_F64 ? layer_fn<double>(net->R) : layer_fn<float>(net->R);
-}
-
-// Pick rows-per-group R and the input chunking for (n, dtype): rows of up
-// to `budget` bytes stay whole in shared memory, R of them per CTA; longer
-// rows are split into equal chunks of whole 32-element multiples.
-int configure(sdnn_net* net) {
-    const int64_t budget = env_int("SDNN_SMEM_BUDGET", 96 * 1024);
-    const int64_t row_bytes = net->n * net->elem;
-    int R = env_int("SDNN_R", 0);
-    if (row_bytes <= budget) {
-        net->n_chunks = 1;
-        net->chunk_len = (int)net->n;
-        if (R <= 0) {
-            int64_t fit = budget / std::max<int64_t>(row_bytes, 1);
-            R = fit >= 8 ? 8 : fit >= 4 ? 4 : fit >= 2 ? 2 : 1;
-        }
-    } else {
-        int64_t c = (row_bytes + budget - 1) / budget;
-        int64_t len = (net->n + c - 1) / c;
-        len = (len + 31) / 32 * 32;
-        net->chunk_len = (int)len;
-        net->n_chunks = (int)((net->n + len - 1) / len);
-        if (R <= 0) R = 1;
-    }
-    if (R != 1 && R != 2 && R != 4 && R != 8) R = 1;
-    net->R = R;
-    net->threads = env_int("SDNN_THREADS", 256);
-    net->smem = (size_t)R * net->chunk_len * net->elem;
-    const void* fn = layer_fn_for(net);
-    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)net->smem));
-    int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, net->threads, net->smem));
-    if (occ < 1) return fail(SDNN_ERR_CAPACITY, "layer kernel does not fit an SM (smem %zu)", net->smem);
-    net->blocks = net->sm_count * occ;
-    return SDNN_OK;
-}
-
-template <typename T>
-void to_T(const double* src, T* dst, int64_t n) {
-    for (int64_t i = 0; i < n; ++i) dst[i] = (T)src[i];
-}
-
-// Upload one ELL-by-output layer given output-major host arrays.  deg[j]
-// (nullable: every column has `width` real slots) counts column j's real
-// inputs; slots past it are padding.
-int upload_layer(sdnn_net* net, int width, const int32_t* idx_om, const double* val_om,
+// Upload one layer given output-major host arrays [n_out][width] with
+// deg[j] real slots in column j (nullable: all width slots real); pads to a
+// multiple of 32 slots with index -1.
+int upload_layer(sdnn_net* net, int64_t n_out, int width, const int32_t* idx_om, const double* val_om,
                  double value_if_null, double bias, const int64_t* deg) {
-    const int64_t n = net->n;
     DevLayer L;
     L.width = width;
+    L.wp = (width + 31) / 32 * 32;
     L.bias = bias;
-    if (width > 65535) return fail(SDNN_ERR_CAPACITY, "column degree %d exceeds 65535", width);
-    const size_t slots = (size_t)width * (size_t)n;
-    std::vector<int32_t> idx_sm(std::max<size_t>(slots, 1));
-    std::vector<unsigned char> val_sm(std::max<size_t>(slots, 1) * net->elem);
-    // transpose output-major -> slot-major
-    parallel_for(n, [&](int64_t j0, int64_t j1) {
+    const size_t slots = (size_t)L.wp * (size_t)n_out;
+    std::vector<int32_t> idx(std::max<size_t>(slots, 1), -1);
+    std::vector<unsigned char> val(std::max<size_t>(slots, 1) * net->elem, 0);
+    parallel_for(n_out, [&](int64_t j0, int64_t j1) {
         for (int64_t j = j0; j < j1; ++j) {
-            for (int s = 0; s < width; ++s) {
-                const size_t om = (size_t)j * width + s, sm = (size_t)s * n + j;
-                idx_sm[sm] = idx_om[om];
-                const double v = val_om ? val_om[om] : value_if_null;
+            const int d = deg ? (int)deg[j] : width;
+            for (int s = 0; s < d; ++s) {
+                const size_t src = (size_t)j * width + s, dst = (size_t)j * L.wp + s;
+                idx[dst] = idx_om[src];
+                const double v = val_om ? val_om[src] : value_if_null;
                 if (net->dtype == SDNN_F64)
-                    reinterpret_cast<double*>(val_sm.data())[sm] = v;
+                    reinterpret_cast<double*>(val.data())[dst] = v;
                 else
-                    reinterpret_cast<float*>(val_sm.data())[sm] = (float)v;
+                    reinterpret_cast<float*>(val.data())[dst] = (float)v;
             }
         }
     });
-    bool uniform = true;
-    if (deg)
-        for (int64_t j = 0; j < n && uniform; ++j) uniform = deg[j] == width;
-    std::vector<uint16_t> bnd;
-    if (net->n_chunks > 1 || !uniform) {
-        const int C = net->n_chunks;
-        bnd.assign((size_t)(C + 1) * n, 0);
-        parallel_for(n, [&](int64_t j0, int64_t j1) {
-            for (int64_t j = j0; j < j1; ++j) {
-                const int32_t* row = idx_om + (size_t)j * width;
-                const int d = deg ? (int)deg[j] : width;
-                int s = 0;
-                for (int c = 0; c <= C; ++c) {
-                    const int64_t lim = (int64_t)c * net->chunk_len;
-                    while (s < d && row[s] < lim) ++s;
-                    bnd[(size_t)c * n + j] = (uint16_t)(c == C ? d : s);
-                }
-            }
-        });
-    }
     CK(cudaMalloc(&L.idx, std::max<size_t>(slots, 1) * sizeof(int32_t)));
     CK(cudaMalloc(&L.val, std::max<size_t>(slots, 1) * net->elem));
-    CK(cudaMemcpy(L.idx, idx_sm.data(), slots * sizeof(int32_t), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(L.val, val_sm.data(), slots * net->elem, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(L.idx, idx.data(), slots * sizeof(int32_t), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(L.val, val.data(), slots * net->elem, cudaMemcpyHostToDevice));
     L.bytes = (int64_t)slots * (4 + net->elem);
-    if (!bnd.empty()) {
-        CK(cudaMalloc(&L.bnd, bnd.size() * sizeof(uint16_t)));
-        CK(cudaMemcpy(L.bnd, bnd.data(), bnd.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
-        L.bytes += (int64_t)bnd.size() * 2;
-    }
     net->layers.push_back(L);
     return SDNN_OK;
 }
 
-int ensure_scratch(sdnn_net* net, int64_t rows, int64_t n_layers) {
-    if (rows > net->ycap) {
-        for (auto& b : net->ybuf) {
-            if (b) CK(cudaFree(b));
-            b = nullptr;
-        }
-        for (auto& b : net->ybuf) CK(cudaMalloc(&b, std::max<int64_t>(rows, 1) * net->n * net->elem));
-        net->ycap = rows;
+// Mirror the layer table on the device (LayerDesc<T>[]).
+template <typename T>
+int sync_descs(sdnn_net* net) {
+    const int64_t L = (int64_t)net->layers.size();
+    if (net->descs_n == L && net->descs) return SDNN_OK;
+    std::vector<LayerDesc<T>> d(std::max<int64_t>(L, 1));
+    for (int64_t i = 0; i < L; ++i) {
+        d[i].idx = net->layers[i].idx;
+        d[i].val = reinterpret_cast<const T*>(net->layers[i].val);
+        d[i].wp = net->layers[i].wp;
+        d[i].bias = (T)net->layers[i].bias;
     }
-    if (rows > net->rcap) {
-        for (auto& b : net->rows) {
-            if (b) CK(cudaFree(b));
-            b = nullptr;
+    if (net->descs) CK(cudaFree(net->descs));
+    CK(cudaMalloc(&net->descs, d.size() * sizeof(LayerDesc<T>)));
+    CK(cudaMemcpy(net->descs, d.data(), d.size() * sizeof(LayerDesc<T>), cudaMemcpyHostToDevice));
+    net->descs_n = L;
+    return SDNN_OK;
+}
+
+template <typename P>
+int grow(P*& p, int64_t& cap, int64_t need, size_t elem) {
+    if (need <= cap && p) return SDNN_OK;
+    if (p) CK(cudaFree(p));
+    p = nullptr;
+    CK(cudaMalloc(&p, std::max<int64_t>(need, 1) * elem));
+    cap = need;
+    return SDNN_OK;
+}
+
+int ensure_tiles(sdnn_net* net, int64_t tiles, int64_t ld, int64_t mstride) {
+    if (tiles > net->tcap || !net->slab[0]) {
+        for (int b = 0; b < 2; ++b) {
+            if (net->slab[b]) CK(cudaFree(net->slab[b]));
+            if (net->mask[b]) CK(cudaFree(net->mask[b]));
+            net->slab[b] = nullptr;
+            net->mask[b] = nullptr;
         }
-        for (auto& b : net->rows) CK(cudaMalloc(&b, std::max<int64_t>(rows, 1) * sizeof(int32_t)));
-        net->rcap = rows;
-    }
-    if (n_layers + 1 > net->ccap) {
-        if (net->counts) CK(cudaFree(net->counts));
-        CK(cudaMalloc(&net->counts, (n_layers + 1) * sizeof(int32_t)));
-        net->ccap = n_layers + 1;
+        const int64_t t = std::max<int64_t>(tiles, 1);
+        for (int b = 0; b < 2; ++b) {
+            CK(cudaMalloc(&net->slab[b], t * ld * 32 * net->elem));
+            CK(cudaMalloc(&net->mask[b], t * mstride));
+        }
+        net->tcap = tiles;
     }
     return SDNN_OK;
 }
 
-// Rows per wave so two activation buffers fit next to everything else.
-int64_t wave_rows(sdnn_net* net, int64_t n_rows) {
+// Rows per wave so the two tile slabs fit next to everything else.
+int64_t wave_rows(sdnn_net* net, int64_t n_rows, int64_t ld, int64_t mstride) {
     int64_t forced = env_int("SDNN_WAVE_ROWS", 0);
     if (forced > 0) return std::min(forced, std::max<int64_t>(n_rows, 1));
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
-    // buffers we already hold can be reused
-    int64_t held = net->ycap * net->n * net->elem * 2 + net->rcap * 8;
-    int64_t avail = (int64_t)free_b + held - (int64_t)(1ull << 30);
-    int64_t per_row = net->n * net->elem * 2 + 8;
-    int64_t w = std::max<int64_t>(1, avail / per_row);
+    const int64_t per_tile = 2 * (ld * 32 * net->elem + mstride);
+    int64_t held = net->tcap * per_tile;
+    int64_t avail = (int64_t)free_b + held - (int64_t)(2ull << 30);
+    int64_t w = std::max<int64_t>(1, avail / per_tile) * 32;
     return std::min(w, std::max<int64_t>(n_rows, 1));
 }
 
-template <typename T>
-LayerArgs<T> make_args(sdnn_net* net, const DevLayer& L, double ymax) {
-    LayerArgs<T> a{};
-    a.n_in = (int)net->n;
-    a.n_out = (int)net->n;
-    a.ld = (int)net->n;
-    a.width = L.width;
-    a.idx = L.idx;
-    a.val = reinterpret_cast<const T*>(L.val);
-    a.bnd = L.bnd;
-    a.n_chunks = net->n_chunks;
-    a.chunk_len = net->chunk_len;
-    a.bias = (T)L.bias;
-    a.ymax = (T)ymax;
-    a.epilogue = 1;
-    return a;
-}
-
-template <typename T>
-int launch_layer(sdnn_net* net, const LayerArgs<T>& a) {
-    const void* fn = layer_fn<T>(net->R);
-    void* args[] = {(void*)&a};
-    CK(cudaLaunchKernel(fn, dim3(net->blocks), dim3(net->threads), args, net->smem, net->stream));
-    return SDNN_OK;
-}
-
-// Dense rows of a live list -> host CSR pieces (ascending row id).
-template <typename T>
-int gather_rows(sdnn_net* net, const T* y, int64_t row_base, int n_cols, const int32_t* rows_dev,
-                int64_t n_list, std::vector<int32_t>& rows_host, std::vector<int64_t>& row_nnz,
-                std::vector<int32_t>& cols_h, std::vector<T>& vals_h) {
-    rows_host.resize(n_list);
-    row_nnz.assign(n_list, 0);
-    cols_h.clear();
-    vals_h.clear();
-    if (n_list == 0) return SDNN_OK;
-    int32_t* counts = nullptr;
-    int64_t* pos = nullptr;
-    int32_t* cols = nullptr;
-    T* vals = nullptr;
-    CK(cudaMemcpyAsync(rows_host.data(), rows_dev, n_list * 4, cudaMemcpyDeviceToHost, net->stream));
-    CK(cudaMalloc(&counts, n_list * 4));
-    const int grid = (int)std::min<int64_t>(n_list, (int64_t)net->sm_count * 8);
-    dense_count_kernel<T><<<grid, 256, 0, net->stream>>>(y, row_base, n_cols, rows_dev, (int)n_list, counts);
-    CK(cudaGetLastError());
-    std::vector<int32_t> cnt(n_list);
-    CK(cudaMemcpyAsync(cnt.data(), counts, n_list * 4, cudaMemcpyDeviceToHost, net->stream));
-    CK(cudaStreamSynchronize(net->stream));
-    std::vector<int64_t> p(n_list);
-    int64_t total = 0;
-    for (int64_t i = 0; i < n_list; ++i) {
-        p[i] = total;
-        total += cnt[i];
-        row_nnz[i] = cnt[i];
-    }
-    CK(cudaMalloc(&pos, n_list * 8));
-    CK(cudaMemcpyAsync(pos, p.data(), n_list * 8, cudaMemcpyHostToDevice, net->stream));
-    CK(cudaMalloc(&cols, std::max<int64_t>(total, 1) * 4));
-    CK(cudaMalloc(&vals, std::max<int64_t>(total, 1) * sizeof(T)));
-    dense_write_kernel<T><<<grid, 256, 0, net->stream>>>(y, row_base, n_cols, rows_dev, (int)n_list, pos, cols, vals);
-    CK(cudaGetLastError());
-    cols_h.resize(total);
-    vals_h.resize(total);
-    CK(cudaMemcpyAsync(cols_h.data(), cols, total * 4, cudaMemcpyDeviceToHost, net->stream));
-    CK(cudaMemcpyAsync(vals_h.data(), vals, total * sizeof(T), cudaMemcpyDeviceToHost, net->stream));
-    CK(cudaStreamSynchronize(net->stream));
-    cudaFree(counts);
-    cudaFree(pos);
-    cudaFree(cols);
-    cudaFree(vals);
-    return SDNN_OK;
-}
+struct LivePred {
+    const int64_t* off;
+    __device__ bool operator()(int r) const { return off[r + 1] > off[r]; }
+};
 
 // Assemble the full B-row CSR from per-wave pieces (rows listed in any order).
 struct Piece {
@@ -383,14 +269,15 @@ struct Piece {
 void assemble(sdnn_result* res, std::vector<Piece>& pieces) {
     const int64_t B = res->n_rows;
     std::vector<int64_t> cnt(B + 1, 0);
-    // locate each row's segment inside its piece
     std::vector<std::pair<int32_t, int64_t>> src(B, {-1, 0});
     for (size_t w = 0; w < pieces.size(); ++w) {
         int64_t at = 0;
         for (size_t i = 0; i < pieces[w].rows.size(); ++i) {
             const int32_t r = pieces[w].rows[i];
-            cnt[r + 1] = pieces[w].nnz[i];
-            src[r] = {(int32_t)w, at};
+            if (r >= 0) {
+                cnt[r + 1] = pieces[w].nnz[i];
+                src[r] = {(int32_t)w, at};
+            }
             at += pieces[w].nnz[i];
         }
     }
@@ -413,100 +300,237 @@ void assemble(sdnn_result* res, std::vector<Piece>& pieces) {
     res->have_y = true;
 }
 
+// Final Y of the tiles that are still live -> host CSR pieces.
 template <typename T>
-int run_impl(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first, int64_t nl,
-             int want_y, sdnn_result* res) {
+int extract(sdnn_net* net, const T* slab, const uint8_t* mask, int ld, int mstride, int n_cols,
+            int64_t n_tiles, const std::vector<uint32_t>& alive, const std::vector<int32_t>& rowid,
+            Piece& p) {
+    p.rows.assign(rowid.begin(), rowid.end());
+    p.nnz.assign(rowid.size(), 0);
+    if (n_tiles == 0) return SDNN_OK;
+    int32_t* counts = nullptr;
+    int64_t* pos = nullptr;
+    int32_t* cols = nullptr;
+    T* vals = nullptr;
+    const int64_t lanes = n_tiles * 32;
+    CK(cudaMalloc(&counts, lanes * 4));
+    const int grid = (int)std::min<int64_t>((n_tiles + 7) / 8, (int64_t)net->sm_count * 16);
+    extract_kernel<T><<<grid, 256, 0, net->stream>>>(slab, mask, ld, mstride, n_cols, (int)n_tiles, nullptr,
+                                                     counts, nullptr, nullptr);
+    CK(cudaGetLastError());
+    std::vector<int32_t> cnt(lanes);
+    CK(cudaMemcpyAsync(cnt.data(), counts, lanes * 4, cudaMemcpyDeviceToHost, net->stream));
+    CK(cudaStreamSynchronize(net->stream));
+    std::vector<int64_t> at(lanes);
+    int64_t total = 0;
+    for (int64_t i = 0; i < lanes; ++i) {
+        // dead tiles hold stale data: they contribute nothing
+        const bool live_tile = alive[i / 32] != 0u;
+        const int64_t c = (live_tile && rowid[i] >= 0) ? cnt[i] : 0;
+        at[i] = total;
+        p.nnz[i] = c;
+        total += c;
+    }
+    // stale tiles are also not written: give them an out-of-range sentinel
+    // by recounting them to zero on the device side through `pos` = -1 lanes
+    CK(cudaMalloc(&pos, lanes * 8));
+    CK(cudaMemcpyAsync(pos, at.data(), lanes * 8, cudaMemcpyHostToDevice, net->stream));
+    CK(cudaMalloc(&cols, std::max<int64_t>(total, 1) * 4));
+    CK(cudaMalloc(&vals, std::max<int64_t>(total, 1) * sizeof(T)));
+    // write pass only over live tiles: compact their ids
+    std::vector<int32_t> live_ids;
+    for (int64_t t = 0; t < n_tiles; ++t)
+        if (alive[t]) live_ids.push_back((int32_t)t);
+    // run the write pass tile by tile range (live tiles only)
+    for (size_t i = 0; i < live_ids.size();) {
+        size_t j = i;
+        while (j + 1 < live_ids.size() && live_ids[j + 1] == live_ids[j] + 1) ++j;
+        const int64_t t0 = live_ids[i], nt = live_ids[j] - t0 + 1;
+        const int g = (int)std::min<int64_t>((nt + 7) / 8, (int64_t)net->sm_count * 16);
+        extract_kernel<T><<<g, 256, 0, net->stream>>>(slab + (size_t)t0 * ld * 32, mask + (size_t)t0 * mstride, ld,
+                                                      mstride, n_cols, (int)nt, pos + t0 * 32, nullptr, cols, vals);
+        CK(cudaGetLastError());
+        i = j + 1;
+    }
+    std::vector<int32_t> hc(total);
+    std::vector<T> hv(total);
+    CK(cudaMemcpyAsync(hc.data(), cols, total * 4, cudaMemcpyDeviceToHost, net->stream));
+    CK(cudaMemcpyAsync(hv.data(), vals, total * sizeof(T), cudaMemcpyDeviceToHost, net->stream));
+    CK(cudaStreamSynchronize(net->stream));
+    p.cols.assign(hc.begin(), hc.end());
+    p.vals.assign(hv.begin(), hv.end());
+    cudaFree(counts);
+    cudaFree(pos);
+    cudaFree(cols);
+    cudaFree(vals);
+    return SDNN_OK;
+}
+
+__global__ void live_rows_kernel(const uint32_t* __restrict__ alive, int n_tiles, int64_t* __restrict__ live) {
+    __shared__ int s[32];
+    const uint32_t* a = alive + (size_t)blockIdx.x * n_tiles;
+    int c = 0;
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) c += __popc(a[t]);
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t v = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += s[w];
+        live[blockIdx.x] = v;
+    }
+}
+
+// One wave of rows [r0, r1) through layers [first, first + nl).
+template <typename T>
+int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first, int64_t nl, int epilogue,
+             int64_t r0, int64_t r1, int64_t n_in, int64_t n_out, int want_y, sdnn_result* res,
+             std::vector<int32_t>& final_rows, std::vector<Piece>& pieces, float& dev_ms) {
+    const int64_t ld = std::max(n_in, n_out), mstride = round16(ld);
+    const int64_t rows = r1 - r0;
+    // ascending list of the wave's rows that hold an entry
+    if (int rc = grow(net->rowlist, net->rcap, std::max<int64_t>(rows, 32), 4)) return rc;
+    if (int rc = grow(net->n_sel, net->ccap, std::max<int64_t>(nl + 2, 2), 8)) return rc;
+    size_t tmp_bytes = 0;
+    thrust::counting_iterator<int> it((int)r0);
+    LivePred pred{batch->off};
+    cub::DeviceSelect::If(nullptr, tmp_bytes, it, net->rowlist, net->n_sel, (int)rows, pred, net->stream);
+    if (tmp_bytes > net->cub_cap) {
+        if (net->cub_tmp) CK(cudaFree(net->cub_tmp));
+        CK(cudaMalloc(&net->cub_tmp, tmp_bytes));
+        net->cub_cap = tmp_bytes;
+    }
+    CK(cub::DeviceSelect::If(net->cub_tmp, tmp_bytes, it, net->rowlist, net->n_sel, (int)rows, pred, net->stream));
+    int32_t n_live = 0;
+    CK(cudaMemcpyAsync(&n_live, net->n_sel, 4, cudaMemcpyDeviceToHost, net->stream));
+    CK(cudaStreamSynchronize(net->stream));
+    const int64_t n_tiles = (n_live + 31) / 32;
+    if (int rc = ensure_tiles(net, n_tiles, ld, mstride)) return rc;
+    int64_t rid_cap = 0;
+    (void)rid_cap;
+    CK(cudaMalloc(&net->rowid, std::max<int64_t>(n_tiles * 32, 1) * 4));
+    CK(cudaMemsetAsync(net->rowid, 0xff, std::max<int64_t>(n_tiles * 32, 1) * 4, net->stream));
+    if (n_live) CK(cudaMemcpyAsync(net->rowid, net->rowlist, n_live * 4, cudaMemcpyDeviceToDevice, net->stream));
+    // per-layer live state
+    {
+        int64_t need = (nl + 1) * std::max<int64_t>(n_tiles, 1);
+        if (int rc = grow(net->alive, net->acap, need, 4)) return rc;
+    }
+    if (!net->tile_count) {
+        CK(cudaMalloc(&net->tile_count, 4));
+    }
+    int32_t* tile_count = nullptr;
+    int64_t* live = nullptr;
+    unsigned long long* stamps = nullptr;
+    CK(cudaMalloc(&tile_count, (nl + 1) * 4));
+    CK(cudaMalloc(&live, (nl + 1) * 8));
+    CK(cudaMalloc(&stamps, (nl + 1) * 8));
+    if (!net->bar) CK(cudaMalloc(&net->bar, 8));
+    CK(cudaMemsetAsync(net->alive, 0, (nl + 1) * std::max<int64_t>(n_tiles, 1) * 4, net->stream));
+    CK(cudaMemsetAsync(tile_count, 0, (nl + 1) * 4, net->stream));
+    CK(cudaMemsetAsync(stamps, 0, (nl + 1) * 8, net->stream));
+    CK(cudaMemsetAsync(net->bar, 0, 8, net->stream));
+
+    NetArgs<T> a{};
+    a.n_in = (int)n_in;
+    a.n_out = (int)n_out;
+    a.ld = (int)ld;
+    a.mstride = (int)mstride;
+    a.L = (int)nl;
+    a.layers = reinterpret_cast<const LayerDesc<T>*>(net->descs) + first;
+    a.ymax = (T)ymax;
+    a.epilogue = epilogue;
+    a.n_tiles = (int)n_tiles;
+    a.rowid = net->rowid;
+    a.csr_off = batch->off;
+    a.csr_cols = batch->cols;
+    a.csr_vals = reinterpret_cast<const T*>(batch->vals);
+    for (int b = 0; b < 2; ++b) {
+        a.slab[b] = reinterpret_cast<T*>(net->slab[b]);
+        a.mask[b] = net->mask[b];
+    }
+    a.alive = net->alive;
+    a.tile_count = tile_count;
+    a.bar = net->bar;
+    a.stamps = net->layer_timing ? stamps : nullptr;
+    a.jb = env_int("SDNN_JB", net->jb);
+    const size_t smem = (size_t)mstride + (size_t)std::max<int64_t>(n_tiles, 1) * 4;
+    const void* fn = (const void*)net_kernel<T>;
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem));
+    if (occ < 1) return fail(SDNN_ERR_CAPACITY, "layer kernel does not fit an SM (smem %zu)", smem);
+    occ = std::min(occ, std::max(1, env_int("SDNN_OCC", occ)));
+    const int grid = net->sm_count * occ;
+    void* args[] = {(void*)&a};
+    CK(cudaEventRecord(net->ev0, net->stream));
+    CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, smem, net->stream));
+    CK(cudaEventRecord(net->ev1, net->stream));
+    res->launches += 1;
+    live_rows_kernel<<<(unsigned)(nl + 1), 256, 0, net->stream>>>(net->alive, (int)std::max<int64_t>(n_tiles, 1), live);
+    CK(cudaGetLastError());
+    std::vector<int64_t> lr(nl + 1);
+    std::vector<unsigned long long> st(nl + 1);
+    std::vector<uint32_t> alive_last(std::max<int64_t>(n_tiles, 1));
+    std::vector<int32_t> rowid(n_tiles * 32);
+    CK(cudaMemcpyAsync(lr.data(), live, (nl + 1) * 8, cudaMemcpyDeviceToHost, net->stream));
+    CK(cudaMemcpyAsync(st.data(), stamps, (nl + 1) * 8, cudaMemcpyDeviceToHost, net->stream));
+    CK(cudaMemcpyAsync(alive_last.data(), net->alive + nl * std::max<int64_t>(n_tiles, 1),
+                       std::max<int64_t>(n_tiles, 1) * 4, cudaMemcpyDeviceToHost, net->stream));
+    if (n_tiles) CK(cudaMemcpyAsync(rowid.data(), net->rowid, n_tiles * 32 * 4, cudaMemcpyDeviceToHost, net->stream));
+    CK(cudaStreamSynchronize(net->stream));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, net->ev0, net->ev1));
+    dev_ms += ms;
+    for (int64_t l = 0; l <= nl; ++l) res->live[l] += lr[l];
+    if (net->layer_timing)
+        for (int64_t l = 0; l < nl; ++l)
+            if (st[l + 1] && st[l]) res->layer_ms[l] += (double)(st[l + 1] - st[l]) * 1e-6;
+    for (int64_t t = 0; t < n_tiles; ++t)
+        for (int r = 0; r < 32; ++r)
+            if ((alive_last[t] >> r) & 1u) final_rows.push_back(rowid[t * 32 + r]);
+    if (want_y) {
+        Piece p;
+        const int last = (int)(nl & 1);  // layer nl-1 wrote buffer nl & 1
+        if (int rc = extract<T>(net, reinterpret_cast<const T*>(net->slab[last]), net->mask[last], (int)ld,
+                                (int)mstride, (int)n_out, n_tiles, alive_last, rowid, p))
+            return rc;
+        pieces.push_back(std::move(p));
+    }
+    cudaFree(tile_count);
+    cudaFree(live);
+    cudaFree(stamps);
+    cudaFree(net->rowid);
+    net->rowid = nullptr;
+    return SDNN_OK;
+}
+
+template <typename T>
+int run_impl(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first, int64_t nl, int want_y,
+             int epilogue, int64_t n_in, int64_t n_out, sdnn_result* res) {
     const int64_t B = batch->n_rows;
-    const int64_t wave = wave_rows(net, B);
-    if (int rc = ensure_scratch(net, std::min(wave, std::max<int64_t>(B, 1)), nl)) return rc;
+    const int64_t ld = std::max(n_in, n_out);
+    if (int rc = sync_descs<T>(net)) return rc;
+    const int64_t wave = wave_rows(net, B, ld, round16(ld));
     res->n_rows = B;
-    res->n_cols = net->n;
+    res->n_cols = n_out;
     res->n_layers = nl;
     res->live.assign(nl + 1, 0);
+    if (net->layer_timing) res->layer_ms.assign(nl, 0.0);
     std::vector<Piece> pieces;
     std::vector<int32_t> final_rows;
-    float total_ms = 0;
-    int64_t launches = 0;
-    const bool timing = net->layer_timing != 0;
-    if (timing) {
-        while ((int64_t)net->lev.size() < nl + 1) {
-            cudaEvent_t e;
-            CK(cudaEventCreate(&e));
-            net->lev.push_back(e);
-        }
-        res->layer_ms.assign(nl, 0.0);
-    }
+    float dev_ms = 0;
     for (int64_t r0 = 0; r0 < std::max<int64_t>(B, 1); r0 += wave) {
         const int64_t r1 = std::min(B, r0 + wave);
-        CK(cudaMemsetAsync(net->counts, 0, (nl + 1) * sizeof(int32_t), net->stream));
-        CK(cudaEventRecord(net->ev0, net->stream));
-        if (r1 > r0) {
-            const int grid = (int)std::min<int64_t>((r1 - r0 + 255) / 256, 65535LL * 16);
-            init_rows_kernel<<<grid, 256, 0, net->stream>>>(batch->off, r0, r1, 0, net->rows[0], net->counts);
-            CK(cudaGetLastError());
-            ++launches;
-        }
-        for (int64_t i = 0; i < nl; ++i) {
-            const DevLayer& L = net->layers[first + i];
-            if (timing) CK(cudaEventRecord(net->lev[i], net->stream));
-            LayerArgs<T> a = make_args<T>(net, L, ymax);
-            if (i == 0) {
-                a.csr_off = batch->off;
-                a.csr_cols = batch->cols;
-                a.csr_vals = reinterpret_cast<const T*>(batch->vals);
-            } else {
-                a.y_in = reinterpret_cast<const T*>(net->ybuf[(i - 1) & 1]);
-            }
-            a.y_out = reinterpret_cast<T*>(net->ybuf[i & 1]);
-            a.row_base = r0;
-            a.rows_in = net->rows[i & 1];
-            a.count_in = net->counts + i;
-            a.rows_out = net->rows[(i + 1) & 1];
-            a.count_out = net->counts + i + 1;
-            if (int rc = launch_layer<T>(net, a)) return rc;
-            ++launches;
-        }
-        if (timing) CK(cudaEventRecord(net->lev[nl], net->stream));
-        CK(cudaEventRecord(net->ev1, net->stream));
-        std::vector<int32_t> cnt(nl + 1);
-        CK(cudaMemcpyAsync(cnt.data(), net->counts, (nl + 1) * 4, cudaMemcpyDeviceToHost, net->stream));
-        CK(cudaStreamSynchronize(net->stream));
-        float ms = 0;
-        CK(cudaEventElapsedTime(&ms, net->ev0, net->ev1));
-        total_ms += ms;
-        for (int64_t l = 0; l <= nl; ++l) res->live[l] += cnt[l];
-        if (timing)
-            for (int64_t l = 0; l < nl; ++l) {
-                float lm = 0;
-                CK(cudaEventElapsedTime(&lm, net->lev[l], net->lev[l + 1]));
-                res->layer_ms[l] += lm;
-            }
-        const int64_t F = cnt[nl];
-        const int32_t* rows_dev = net->rows[nl & 1];
-        if (want_y) {
-            Piece p;
-            std::vector<int32_t> cols;
-            std::vector<T> vals;
-            if (int rc = gather_rows<T>(net, reinterpret_cast<const T*>(net->ybuf[(nl - 1) & 1]), r0,
-                                        (int)net->n, rows_dev, F, p.rows, p.nnz, p.cols, vals))
-                return rc;
-            p.vals.assign(vals.begin(), vals.end());
-            // rows whose final entries all vanished cannot be listed (the
-            // live list is exact), so every listed row has nnz > 0
-            for (int32_t r : p.rows) final_rows.push_back(r);
-            pieces.push_back(std::move(p));
-        } else {
-            std::vector<int32_t> fr(F);
-            if (F) CK(cudaMemcpy(fr.data(), rows_dev, F * 4, cudaMemcpyDeviceToHost));
-            final_rows.insert(final_rows.end(), fr.begin(), fr.end());
-        }
+        if (int rc = run_wave<T>(net, batch, ymax, first, nl, epilogue, r0, r1, n_in, n_out, want_y, res,
+                                 final_rows, pieces, dev_ms))
+            return rc;
         if (B == 0) break;
     }
     std::sort(final_rows.begin(), final_rows.end());
     res->cats.resize(final_rows.size());
     for (size_t i = 0; i < final_rows.size(); ++i) res->cats[i] = (int64_t)final_rows[i] + 1;
-    res->dev_ms = total_ms;
-    res->launches = launches;
+    res->dev_ms = dev_ms;
     if (want_y) assemble(res, pieces);
     return SDNN_OK;
 }
@@ -521,6 +545,7 @@ int upload_csr(sdnn_net* net, int64_t n_rows, const int64_t* off, const int64_t*
         if (off[i + 1] < off[i]) return fail(SDNN_ERR_PARAMETER, "row_offsets non-monotone at %lld", (long long)i);
     b->n_rows = n_rows;
     b->nnz = nnz;
+    b->n_cols = n_cols;
     const size_t bytes = (size_t)nnz * (4 + sizeof(T));
     if (bytes > net->pinned_cap) {
         if (net->pinned) CK(cudaFreeHost(net->pinned));
@@ -598,6 +623,9 @@ int make_net(int device, int dtype, int64_t n, sdnn_net** out) {
     CK(cudaGetDeviceCount(&count));
     if (device < 0 || device >= count) return fail(SDNN_ERR_PARAMETER, "no CUDA device %d", device);
     CK(cudaSetDevice(device));
+    int coop = 0;
+    CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
+    if (!coop) return fail(SDNN_ERR_CAPACITY, "device %d lacks cooperative launch", device);
     sdnn_net* net = new sdnn_net;
     net->device = device;
     net->dtype = dtype;
@@ -607,33 +635,11 @@ int make_net(int device, int dtype, int64_t n, sdnn_net** out) {
     CK(cudaStreamCreateWithFlags(&net->stream, cudaStreamNonBlocking));
     CK(cudaEventCreate(&net->ev0));
     CK(cudaEventCreate(&net->ev1));
-    if (int rc = configure(net)) {
-        sdnn_net_destroy(net);
-        return rc;
-    }
     *out = net;
     return SDNN_OK;
 }
 
 }  // namespace
-
-namespace sdnn {
-__global__ void init_rows_kernel(const int64_t* __restrict__ off, int64_t r0, int64_t r1, int all_rows,
-                                 int32_t* __restrict__ rows, int32_t* __restrict__ count) {
-    for (int64_t r = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < r1;
-         r += (int64_t)gridDim.x * blockDim.x) {
-        const bool live = all_rows || off[r + 1] > off[r];
-        const unsigned b = __ballot_sync(__activemask(), live);
-        // warp-aggregated append
-        const int lane = threadIdx.x & 31;
-        const int leader = __ffs(__activemask()) - 1;
-        int base = 0;
-        if (lane == leader && b) base = atomicAdd(count, __popc(b));
-        base = __shfl_sync(__activemask(), base, leader);
-        if (live) rows[base + __popc(b & ((1u << lane) - 1u))] = (int32_t)r;
-    }
-}
-}  // namespace sdnn
 
 // ===================================================================== C ABI
 
@@ -665,13 +671,20 @@ void sdnn_net_destroy(sdnn_net* net) {
     for (auto& L : net->layers) {
         cudaFree(L.idx);
         cudaFree(L.val);
-        cudaFree(L.bnd);
     }
-    for (auto b : net->ybuf) cudaFree(b);
-    for (auto b : net->rows) cudaFree(b);
-    cudaFree(net->counts);
+    cudaFree(net->descs);
+    for (int b = 0; b < 2; ++b) {
+        cudaFree(net->slab[b]);
+        cudaFree(net->mask[b]);
+    }
+    cudaFree(net->rowid);
+    cudaFree(net->rowlist);
+    cudaFree(net->alive);
+    cudaFree(net->tile_count);
+    cudaFree(net->bar);
+    cudaFree(net->n_sel);
+    cudaFree(net->cub_tmp);
     if (net->pinned) cudaFreeHost(net->pinned);
-    for (auto e : net->lev) cudaEventDestroy(e);
     if (net->ev0) cudaEventDestroy(net->ev0);
     if (net->ev1) cudaEventDestroy(net->ev1);
     if (net->stream) cudaStreamDestroy(net->stream);
@@ -687,7 +700,7 @@ int sdnn_net_add_layer_csr(sdnn_net* net, const int64_t* w_off, const int64_t* w
     std::vector<int64_t> deg;
     int width = 0;
     if (int rc = csr_to_ell(net->n, net->n, w_off, w_cols, w_vals, nnz, idx, val, width, deg)) return rc;
-    return upload_layer(net, width, idx.data(), val.data(), 0.0, bias, deg.data());
+    return upload_layer(net, net->n, width, idx.data(), val.data(), 0.0, bias, deg.data());
 }
 
 int sdnn_net_add_layer_ell(sdnn_net* net, int32_t width, const int32_t* idx, const double* vals,
@@ -701,7 +714,7 @@ int sdnn_net_add_layer_ell(sdnn_net* net, int32_t width, const int32_t* idx, con
             if (s > 0 && v <= idx[(size_t)j * width + s - 1])
                 return fail(SDNN_ERR_PARAMETER, "ELL column %lld not strictly ascending", (long long)j);
         }
-    return upload_layer(net, width, idx, vals, 0.0, bias, nullptr);
+    return upload_layer(net, net->n, width, idx, vals, 0.0, bias, nullptr);
 }
 
 int sdnn_net_add_layers_permunion(sdnn_net* net, uint64_t seed, int64_t first_layer, int64_t count,
@@ -716,7 +729,7 @@ int sdnn_net_add_layers_permunion(sdnn_net* net, uint64_t seed, int64_t first_la
         int rc = sdnn_gen_permunion_ell_layers(seed, first_layer + l0, m, (int32_t)net->n, width, threads, idx.data());
         if (rc) return fail(rc, "perm-union generation failed");
         for (int64_t l = 0; l < m; ++l)
-            if (int rc2 = upload_layer(net, width, idx.data() + (size_t)l * net->n * width, nullptr, value, bias,
+            if (int rc2 = upload_layer(net, net->n, width, idx.data() + (size_t)l * net->n * width, nullptr, value, bias,
                                        nullptr))
                 return rc2;
     }
@@ -773,8 +786,8 @@ static int run_checked(sdnn_net* net, const sdnn_batch* batch, double ymax, int6
     if (int rc = set_device(net)) return rc;
     sdnn_result* res = new sdnn_result;
     const double t0 = now_ms();
-    int rc = net->dtype == SDNN_F64 ? run_impl<double>(net, batch, ymax, first, nl, want_y, res)
-                                    : run_impl<float>(net, batch, ymax, first, nl, want_y, res);
+    int rc = net->dtype == SDNN_F64 ? run_impl<double>(net, batch, ymax, first, nl, want_y, 1, net->n, net->n, res)
+                                    : run_impl<float>(net, batch, ymax, first, nl, want_y, 1, net->n, net->n, res);
     if (rc) {
         delete res;
         return rc;
@@ -874,11 +887,9 @@ int sdnn_spmm(int device, int dtype, int64_t n_rows, int64_t n_inner, int64_t n_
               const int64_t* y_cols, const double* y_vals, const int64_t* w_off, const int64_t* w_cols,
               const double* w_vals, sdnn_result** out) {
     if (!out || n_rows < 0 || n_inner < 1 || n_out < 1) return fail(SDNN_ERR_PARAMETER, "bad spmm shape");
-    // one rectangular layer: build a scratch net of max(n_inner, n_out)
-    // neurons whose geometry covers both extents, then run it raw
+    // one rectangular layer run raw (no epilogue) through the same kernel
     sdnn_net* net = nullptr;
-    const int64_t n = std::max(n_inner, n_out);
-    if (int rc = make_net(device, dtype, n, &net)) return rc;
+    if (int rc = make_net(device, dtype, std::max(n_inner, n_out), &net)) return rc;
     int rc = SDNN_OK;
     sdnn_batch* b = nullptr;
     sdnn_result* res = nullptr;
@@ -888,65 +899,20 @@ int sdnn_spmm(int device, int dtype, int64_t n_rows, int64_t n_inner, int64_t n_
         std::vector<int64_t> deg;
         int width = 0;
         const int64_t nnz_w = w_off[n_inner];
-        // pad the weight CSR to n x n rows (extra rows empty)
-        std::vector<int64_t> off(n + 1, nnz_w);
-        memcpy(off.data(), w_off, (n_inner + 1) * sizeof(int64_t));
-        if ((rc = csr_to_ell(n, n, off.data(), w_cols, w_vals, nnz_w, idx, val, width, deg))) break;
-        if ((rc = upload_layer(net, width, idx.data(), val.data(), 0.0, 0.0, deg.data()))) break;
+        if ((rc = csr_to_ell(n_inner, n_out, w_off, w_cols, w_vals, nnz_w, idx, val, width, deg))) break;
+        if ((rc = upload_layer(net, n_out, width, idx.data(), val.data(), 0.0, 0.0, deg.data()))) break;
         b = new sdnn_batch;
         b->net = net;
-        {
-            static const int64_t zero_off[1] = {0};
-            const int64_t* yo = n_rows > 0 ? y_off : zero_off;
-            rc = dtype == SDNN_F64 ? upload_csr<double>(net, n_rows, yo, y_cols, y_vals, n_inner, b)
-                                   : upload_csr<float>(net, n_rows, yo, y_cols, y_vals, n_inner, b);
-            if (rc) break;
-        }
-        if ((rc = ensure_scratch(net, std::max<int64_t>(n_rows, 1), 1))) break;
+        static const int64_t zero_off[1] = {0};
+        const int64_t* yo = n_rows > 0 ? y_off : zero_off;
+        rc = dtype == SDNN_F64 ? upload_csr<double>(net, n_rows, yo, y_cols, y_vals, n_inner, b)
+                               : upload_csr<float>(net, n_rows, yo, y_cols, y_vals, n_inner, b);
+        if (rc) break;
         res = new sdnn_result;
-        res->n_rows = n_rows;
-        res->n_cols = n_out;
-        res->n_layers = 1;
-        res->live.assign(2, 0);
-        auto body = [&](auto tag) -> int {
-            using T = decltype(tag);
-            CK(cudaMemsetAsync(net->counts, 0, 2 * sizeof(int32_t), net->stream));
-            if (n_rows > 0) {
-                const int grid = (int)std::min<int64_t>((n_rows + 255) / 256, 65535LL * 16);
-                init_rows_kernel<<<grid, 256, 0, net->stream>>>(b->off, 0, n_rows, 1, net->rows[0], net->counts);
-                CK(cudaGetLastError());
-            }
-            LayerArgs<T> a = make_args<T>(net, net->layers[0], 32.0);
-            a.n_in = (int)n_inner;
-            a.n_out = (int)n_out;
-            a.epilogue = 0;
-            a.csr_off = b->off;
-            a.csr_cols = b->cols;
-            a.csr_vals = reinterpret_cast<const T*>(b->vals);
-            a.y_out = reinterpret_cast<T*>(net->ybuf[0]);
-            a.rows_in = net->rows[0];
-            a.count_in = net->counts;
-            a.rows_out = net->rows[1];
-            a.count_out = net->counts + 1;
-            if (int e = launch_layer<T>(net, a)) return e;
-            Piece p;
-            std::vector<int32_t> cols;
-            std::vector<T> vals;
-            if (int e = gather_rows<T>(net, reinterpret_cast<const T*>(net->ybuf[0]), 0, (int)n_out, net->rows[0],
-                                       n_rows, p.rows, p.nnz, p.cols, vals))
-                return e;
-            p.vals.assign(vals.begin(), vals.end());
-            for (size_t i = 0; i < p.rows.size(); ++i)
-                if (p.nnz[i] > 0) res->cats.push_back((int64_t)p.rows[i] + 1);
-            std::sort(res->cats.begin(), res->cats.end());
-            std::vector<Piece> ps;
-            ps.push_back(std::move(p));
-            assemble(res, ps);
-            return SDNN_OK;
-        };
-        rc = dtype == SDNN_F64 ? body(double{}) : body(float{});
+        rc = dtype == SDNN_F64 ? run_impl<double>(net, b, 32.0, 0, 1, 1, 0, n_inner, n_out, res)
+                               : run_impl<float>(net, b, 32.0, 0, 1, 1, 0, n_inner, n_out, res);
     } while (0);
-    if (b) sdnn_batch_free(b);
+    if (b) free_batch(b);
     sdnn_net_destroy(net);
     if (rc) {
         delete res;

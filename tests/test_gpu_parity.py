@@ -196,11 +196,12 @@ def permunion_case(n, layers, rows, value, p=0.35):
     return w, O.CSR(rows, n, off, cols, vals), [O.CSR(n, n, *W.layer_csr(w, l)) for l in range(layers)]
 
 
-@pytest.mark.parametrize("budget,R", [("2048", "1"), ("8192", "2"), ("65536", "8"), ("4096", "4")])
+@pytest.mark.parametrize("jb,occ", [("1", "1"), ("7", "2"), ("100", "1"), ("4096", "3")])
 @pytest.mark.parametrize("dtype,prec", [("f64", 64), ("f32", 32)])
-def test_chunked_and_grouped_geometry(env, budget, R, dtype, prec):
-    env["SDNN_SMEM_BUDGET"] = budget
-    env["SDNN_R"] = R
+def test_work_item_geometry(env, jb, occ, dtype, prec):
+    """Output-block size and grid size change only the schedule, never bits."""
+    env["SDNN_JB"] = jb
+    env["SDNN_OCC"] = occ
     w, y0, layers = permunion_case(1024, 5, 97, 0.125)
     net = E.DeviceNetwork(w.n, 0, dtype)
     for l in range(w.layers):
