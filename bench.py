@@ -332,6 +332,7 @@ def run_ours(args, dist: Dist):
             "per_launch_ms": float(prof.layer_ms[dom]),
             "algorithmic_bytes": float(lb[dom]),
             "all_live_launches_gbs": all_gbs,
+            "live_layer_ms": [round(float(prof.layer_ms[l]), 3) for l in live_layers[:8]],
             "peak_kind": peak_kind,
         },
         "e2e": {

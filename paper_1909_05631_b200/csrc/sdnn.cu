@@ -110,6 +110,7 @@ struct sdnn_net {
     void* slab[2] = {nullptr, nullptr};
     uint8_t* mask[2] = {nullptr, nullptr};
     int64_t tcap = 0;  // tiles per buffer
+    int64_t tcap_lines = 0;
     int32_t* rowid = nullptr;
     int32_t* rowlist = nullptr;
     int64_t rcap = 0;
@@ -156,7 +157,6 @@ int set_device(const sdnn_net* net) {
     return SDNN_OK;
 }
 
-int64_t round16(int64_t x) { return (x + 15) / 16 * 16; }
 
 // Upload one layer given output-major host arrays [n_out][width] with
 // deg[j] real slots in column j (nullable: all width slots real); pads to a
@@ -222,34 +222,35 @@ int grow(P*& p, int64_t& cap, int64_t need, size_t elem) {
     return SDNN_OK;
 }
 
-int ensure_tiles(sdnn_net* net, int64_t tiles, int64_t ld, int64_t mstride) {
-    if (tiles > net->tcap || !net->slab[0]) {
+int ensure_tiles(sdnn_net* net, int64_t tiles, int64_t ld) {
+    if (tiles > net->tcap || !net->slab[0] || ld * std::max<int64_t>(tiles, 1) > net->tcap_lines) {
         for (int b = 0; b < 2; ++b) {
             if (net->slab[b]) CK(cudaFree(net->slab[b]));
             if (net->mask[b]) CK(cudaFree(net->mask[b]));
             net->slab[b] = nullptr;
             net->mask[b] = nullptr;
         }
-        const int64_t t = std::max<int64_t>(tiles, 1);
+        const int64_t lines = std::max<int64_t>(tiles, 1) * ld;
         for (int b = 0; b < 2; ++b) {
-            CK(cudaMalloc(&net->slab[b], t * ld * 32 * net->elem));
-            CK(cudaMalloc(&net->mask[b], t * mstride));
+            CK(cudaMalloc(&net->slab[b], lines * kLineBytes));
+            CK(cudaMalloc(&net->mask[b], lines));
         }
         net->tcap = tiles;
+        net->tcap_lines = lines;
     }
     return SDNN_OK;
 }
 
 // Rows per wave so the two tile slabs fit next to everything else.
-int64_t wave_rows(sdnn_net* net, int64_t n_rows, int64_t ld, int64_t mstride) {
+int64_t wave_rows(sdnn_net* net, int64_t n_rows, int64_t ld, int tr) {
     int64_t forced = env_int("SDNN_WAVE_ROWS", 0);
     if (forced > 0) return std::min(forced, std::max<int64_t>(n_rows, 1));
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
-    const int64_t per_tile = 2 * (ld * 32 * net->elem + mstride);
-    int64_t held = net->tcap * per_tile;
+    const int64_t per_tile = 2 * ld * (kLineBytes + 1);
+    int64_t held = net->tcap_lines * (kLineBytes + 1) * 2;
     int64_t avail = (int64_t)free_b + held - (int64_t)(2ull << 30);
-    int64_t w = std::max<int64_t>(1, avail / per_tile) * 32;
+    int64_t w = std::max<int64_t>(1, avail / per_tile) * tr;
     return std::min(w, std::max<int64_t>(n_rows, 1));
 }
 
@@ -302,9 +303,9 @@ void assemble(sdnn_result* res, std::vector<Piece>& pieces) {
 
 // Final Y of the tiles that are still live -> host CSR pieces.
 template <typename T>
-int extract(sdnn_net* net, const T* slab, const uint8_t* mask, int ld, int mstride, int n_cols,
-            int64_t n_tiles, const std::vector<uint32_t>& alive, const std::vector<int32_t>& rowid,
-            Piece& p) {
+int extract(sdnn_net* net, const T* slab, const uint8_t* mask, int ld, int n_cols, int64_t n_tiles,
+            const std::vector<uint32_t>& alive, const std::vector<int32_t>& rowid, Piece& p) {
+    constexpr int TR = tile_rows<T>(), AW = alive_words<T>(), RPL = rows_per_lane<T>();
     p.rows.assign(rowid.begin(), rowid.end());
     p.nnz.assign(rowid.size(), 0);
     if (n_tiles == 0) return SDNN_OK;
@@ -312,11 +313,11 @@ int extract(sdnn_net* net, const T* slab, const uint8_t* mask, int ld, int mstri
     int64_t* pos = nullptr;
     int32_t* cols = nullptr;
     T* vals = nullptr;
-    const int64_t lanes = n_tiles * 32;
+    const int64_t lanes = n_tiles * TR;
     CK(cudaMalloc(&counts, lanes * 4));
     const int grid = (int)std::min<int64_t>((n_tiles + 7) / 8, (int64_t)net->sm_count * 16);
-    extract_kernel<T><<<grid, 256, 0, net->stream>>>(slab, mask, ld, mstride, n_cols, (int)n_tiles, nullptr,
-                                                     counts, nullptr, nullptr);
+    extract_kernel<T><<<grid, 256, 0, net->stream>>>(slab, mask, ld, n_cols, (int)n_tiles, nullptr, counts,
+                                                     nullptr, nullptr);
     CK(cudaGetLastError());
     std::vector<int32_t> cnt(lanes);
     CK(cudaMemcpyAsync(cnt.data(), counts, lanes * 4, cudaMemcpyDeviceToHost, net->stream));
@@ -324,31 +325,30 @@ int extract(sdnn_net* net, const T* slab, const uint8_t* mask, int ld, int mstri
     std::vector<int64_t> at(lanes);
     int64_t total = 0;
     for (int64_t i = 0; i < lanes; ++i) {
-        // dead tiles hold stale data: they contribute nothing
-        const bool live_tile = alive[i / 32] != 0u;
-        const int64_t c = (live_tile && rowid[i] >= 0) ? cnt[i] : 0;
+        const int64_t t = i / TR;
+        const int r = (int)(i % TR);
+        // a row counts only if it is live at the end; dead tiles hold stale data
+        const bool live = (alive[t * AW + r % RPL] >> (r / RPL)) & 1u;
+        const int64_t c = (live && rowid[i] >= 0) ? cnt[i] : 0;
         at[i] = total;
         p.nnz[i] = c;
         total += c;
     }
-    // stale tiles are also not written: give them an out-of-range sentinel
-    // by recounting them to zero on the device side through `pos` = -1 lanes
     CK(cudaMalloc(&pos, lanes * 8));
     CK(cudaMemcpyAsync(pos, at.data(), lanes * 8, cudaMemcpyHostToDevice, net->stream));
     CK(cudaMalloc(&cols, std::max<int64_t>(total, 1) * 4));
     CK(cudaMalloc(&vals, std::max<int64_t>(total, 1) * sizeof(T)));
-    // write pass only over live tiles: compact their ids
+    // write pass over runs of consecutive live tiles only
     std::vector<int32_t> live_ids;
     for (int64_t t = 0; t < n_tiles; ++t)
-        if (alive[t]) live_ids.push_back((int32_t)t);
-    // run the write pass tile by tile range (live tiles only)
+        if (alive[t * AW + RPL]) live_ids.push_back((int32_t)t);
     for (size_t i = 0; i < live_ids.size();) {
         size_t j = i;
         while (j + 1 < live_ids.size() && live_ids[j + 1] == live_ids[j] + 1) ++j;
         const int64_t t0 = live_ids[i], nt = live_ids[j] - t0 + 1;
         const int g = (int)std::min<int64_t>((nt + 7) / 8, (int64_t)net->sm_count * 16);
-        extract_kernel<T><<<g, 256, 0, net->stream>>>(slab + (size_t)t0 * ld * 32, mask + (size_t)t0 * mstride, ld,
-                                                      mstride, n_cols, (int)nt, pos + t0 * 32, nullptr, cols, vals);
+        extract_kernel<T><<<g, 256, 0, net->stream>>>(slab + (size_t)t0 * ld * TR, mask + (size_t)t0 * ld, ld, n_cols,
+                                                      (int)nt, pos + t0 * TR, nullptr, cols, vals);
         CK(cudaGetLastError());
         i = j + 1;
     }
@@ -357,6 +357,9 @@ int extract(sdnn_net* net, const T* slab, const uint8_t* mask, int ld, int mstri
     CK(cudaMemcpyAsync(hc.data(), cols, total * 4, cudaMemcpyDeviceToHost, net->stream));
     CK(cudaMemcpyAsync(hv.data(), vals, total * sizeof(T), cudaMemcpyDeviceToHost, net->stream));
     CK(cudaStreamSynchronize(net->stream));
+    // rows that are not live keep nnz 0 and are excluded from the write pass,
+    // but a live row's count may include stale dead-row slots: none exist,
+    // because extraction only reads rows flagged live
     p.cols.assign(hc.begin(), hc.end());
     p.vals.assign(hv.begin(), hv.end());
     cudaFree(counts);
@@ -366,11 +369,13 @@ int extract(sdnn_net* net, const T* slab, const uint8_t* mask, int ld, int mstri
     return SDNN_OK;
 }
 
-__global__ void live_rows_kernel(const uint32_t* __restrict__ alive, int n_tiles, int64_t* __restrict__ live) {
+// Live rows per layer: popcount of the per-lane words (not the tile flag).
+__global__ void live_rows_kernel(const uint32_t* __restrict__ alive, int n_tiles, int aw, int64_t* __restrict__ live) {
     __shared__ int s[32];
-    const uint32_t* a = alive + (size_t)blockIdx.x * n_tiles;
+    const uint32_t* a = alive + (size_t)blockIdx.x * n_tiles * aw;
     int c = 0;
-    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) c += __popc(a[t]);
+    for (int i = threadIdx.x; i < n_tiles * aw; i += blockDim.x)
+        if (i % aw != aw - 1) c += __popc(a[i]);
     for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
     if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
     __syncthreads();
@@ -386,10 +391,11 @@ template <typename T>
 int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first, int64_t nl, int epilogue,
              int64_t r0, int64_t r1, int64_t n_in, int64_t n_out, int want_y, sdnn_result* res,
              std::vector<int32_t>& final_rows, std::vector<Piece>& pieces, float& dev_ms) {
-    const int64_t ld = std::max(n_in, n_out), mstride = round16(ld);
+    constexpr int TR = tile_rows<T>(), RPL = rows_per_lane<T>(), AW = alive_words<T>();
+    const int64_t ld = std::max(n_in, n_out) + 1;  // + the zero line
     const int64_t rows = r1 - r0;
     // ascending list of the wave's rows that hold an entry
-    if (int rc = grow(net->rowlist, net->rcap, std::max<int64_t>(rows, 32), 4)) return rc;
+    if (int rc = grow(net->rowlist, net->rcap, std::max<int64_t>(rows, TR), 4)) return rc;
     if (int rc = grow(net->n_sel, net->ccap, std::max<int64_t>(nl + 2, 2), 8)) return rc;
     size_t tmp_bytes = 0;
     thrust::counting_iterator<int> it((int)r0);
@@ -404,21 +410,13 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     int32_t n_live = 0;
     CK(cudaMemcpyAsync(&n_live, net->n_sel, 4, cudaMemcpyDeviceToHost, net->stream));
     CK(cudaStreamSynchronize(net->stream));
-    const int64_t n_tiles = (n_live + 31) / 32;
-    if (int rc = ensure_tiles(net, n_tiles, ld, mstride)) return rc;
-    int64_t rid_cap = 0;
-    (void)rid_cap;
-    CK(cudaMalloc(&net->rowid, std::max<int64_t>(n_tiles * 32, 1) * 4));
-    CK(cudaMemsetAsync(net->rowid, 0xff, std::max<int64_t>(n_tiles * 32, 1) * 4, net->stream));
+    const int64_t n_tiles = (n_live + TR - 1) / TR;
+    if (int rc = ensure_tiles(net, n_tiles, ld)) return rc;
+    CK(cudaMalloc(&net->rowid, std::max<int64_t>(n_tiles * TR, 1) * 4));
+    CK(cudaMemsetAsync(net->rowid, 0xff, std::max<int64_t>(n_tiles * TR, 1) * 4, net->stream));
     if (n_live) CK(cudaMemcpyAsync(net->rowid, net->rowlist, n_live * 4, cudaMemcpyDeviceToDevice, net->stream));
-    // per-layer live state
-    {
-        int64_t need = (nl + 1) * std::max<int64_t>(n_tiles, 1);
-        if (int rc = grow(net->alive, net->acap, need, 4)) return rc;
-    }
-    if (!net->tile_count) {
-        CK(cudaMalloc(&net->tile_count, 4));
-    }
+    const int64_t tiles1 = std::max<int64_t>(n_tiles, 1);
+    if (int rc = grow(net->alive, net->acap, (nl + 1) * tiles1 * AW, 4)) return rc;
     int32_t* tile_count = nullptr;
     int64_t* live = nullptr;
     unsigned long long* stamps = nullptr;
@@ -426,7 +424,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     CK(cudaMalloc(&live, (nl + 1) * 8));
     CK(cudaMalloc(&stamps, (nl + 1) * 8));
     if (!net->bar) CK(cudaMalloc(&net->bar, 8));
-    CK(cudaMemsetAsync(net->alive, 0, (nl + 1) * std::max<int64_t>(n_tiles, 1) * 4, net->stream));
+    CK(cudaMemsetAsync(net->alive, 0, (nl + 1) * tiles1 * AW * 4, net->stream));
     CK(cudaMemsetAsync(tile_count, 0, (nl + 1) * 4, net->stream));
     CK(cudaMemsetAsync(stamps, 0, (nl + 1) * 8, net->stream));
     CK(cudaMemsetAsync(net->bar, 0, 8, net->stream));
@@ -435,16 +433,11 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     a.n_in = (int)n_in;
     a.n_out = (int)n_out;
     a.ld = (int)ld;
-    a.mstride = (int)mstride;
     a.L = (int)nl;
     a.layers = reinterpret_cast<const LayerDesc<T>*>(net->descs) + first;
     a.ymax = (T)ymax;
     a.epilogue = epilogue;
     a.n_tiles = (int)n_tiles;
-    a.rowid = net->rowid;
-    a.csr_off = batch->off;
-    a.csr_cols = batch->cols;
-    a.csr_vals = reinterpret_cast<const T*>(batch->vals);
     for (int b = 0; b < 2; ++b) {
         a.slab[b] = reinterpret_cast<T*>(net->slab[b]);
         a.mask[b] = net->mask[b];
@@ -454,7 +447,10 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     a.bar = net->bar;
     a.stamps = net->layer_timing ? stamps : nullptr;
     a.jb = env_int("SDNN_JB", net->jb);
-    const size_t smem = (size_t)mstride + (size_t)std::max<int64_t>(n_tiles, 1) * 4;
+    const size_t dsmem = (size_t)(n_in + 3) / 4 * 4;
+    const void* dfn = (const void*)densify_kernel<T>;
+    CK(cudaFuncSetAttribute(dfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
+    const size_t smem = (size_t)tiles1 * 4;
     const void* fn = (const void*)net_kernel<T>;
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
@@ -464,20 +460,28 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     const int grid = net->sm_count * occ;
     void* args[] = {(void*)&a};
     CK(cudaEventRecord(net->ev0, net->stream));
+    if (n_tiles) {
+        const int dgrid = (int)std::min<int64_t>(n_tiles, (int64_t)net->sm_count * 4);
+        densify_kernel<T><<<dgrid, 512, dsmem, net->stream>>>(
+            batch->off, batch->cols, reinterpret_cast<const T*>(batch->vals), net->rowid, (int)n_in, (int)ld,
+            (int)n_tiles, a.slab[0], a.slab[1], a.mask[0], net->alive, tile_count);
+        CK(cudaGetLastError());
+        res->launches += 1;
+    }
     CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, smem, net->stream));
     CK(cudaEventRecord(net->ev1, net->stream));
     res->launches += 1;
-    live_rows_kernel<<<(unsigned)(nl + 1), 256, 0, net->stream>>>(net->alive, (int)std::max<int64_t>(n_tiles, 1), live);
+    live_rows_kernel<<<(unsigned)(nl + 1), 256, 0, net->stream>>>(net->alive, (int)tiles1, AW, live);
     CK(cudaGetLastError());
     std::vector<int64_t> lr(nl + 1);
     std::vector<unsigned long long> st(nl + 1);
-    std::vector<uint32_t> alive_last(std::max<int64_t>(n_tiles, 1));
-    std::vector<int32_t> rowid(n_tiles * 32);
+    std::vector<uint32_t> alive_last(tiles1 * AW);
+    std::vector<int32_t> rowid(n_tiles * TR);
     CK(cudaMemcpyAsync(lr.data(), live, (nl + 1) * 8, cudaMemcpyDeviceToHost, net->stream));
     CK(cudaMemcpyAsync(st.data(), stamps, (nl + 1) * 8, cudaMemcpyDeviceToHost, net->stream));
-    CK(cudaMemcpyAsync(alive_last.data(), net->alive + nl * std::max<int64_t>(n_tiles, 1),
-                       std::max<int64_t>(n_tiles, 1) * 4, cudaMemcpyDeviceToHost, net->stream));
-    if (n_tiles) CK(cudaMemcpyAsync(rowid.data(), net->rowid, n_tiles * 32 * 4, cudaMemcpyDeviceToHost, net->stream));
+    CK(cudaMemcpyAsync(alive_last.data(), net->alive + nl * tiles1 * AW, tiles1 * AW * 4, cudaMemcpyDeviceToHost,
+                       net->stream));
+    if (n_tiles) CK(cudaMemcpyAsync(rowid.data(), net->rowid, n_tiles * TR * 4, cudaMemcpyDeviceToHost, net->stream));
     CK(cudaStreamSynchronize(net->stream));
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, net->ev0, net->ev1));
@@ -487,13 +491,13 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
         for (int64_t l = 0; l < nl; ++l)
             if (st[l + 1] && st[l]) res->layer_ms[l] += (double)(st[l + 1] - st[l]) * 1e-6;
     for (int64_t t = 0; t < n_tiles; ++t)
-        for (int r = 0; r < 32; ++r)
-            if ((alive_last[t] >> r) & 1u) final_rows.push_back(rowid[t * 32 + r]);
+        for (int r = 0; r < TR; ++r)
+            if ((alive_last[t * AW + r % RPL] >> (r / RPL)) & 1u) final_rows.push_back(rowid[t * TR + r]);
     if (want_y) {
         Piece p;
         const int last = (int)(nl & 1);  // layer nl-1 wrote buffer nl & 1
         if (int rc = extract<T>(net, reinterpret_cast<const T*>(net->slab[last]), net->mask[last], (int)ld,
-                                (int)mstride, (int)n_out, n_tiles, alive_last, rowid, p))
+                                (int)n_out, n_tiles, alive_last, rowid, p))
             return rc;
         pieces.push_back(std::move(p));
     }
@@ -509,9 +513,9 @@ template <typename T>
 int run_impl(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first, int64_t nl, int want_y,
              int epilogue, int64_t n_in, int64_t n_out, sdnn_result* res) {
     const int64_t B = batch->n_rows;
-    const int64_t ld = std::max(n_in, n_out);
+    const int64_t ld = std::max(n_in, n_out) + 1;
     if (int rc = sync_descs<T>(net)) return rc;
-    const int64_t wave = wave_rows(net, B, ld, round16(ld));
+    const int64_t wave = wave_rows(net, B, ld, tile_rows<T>());
     res->n_rows = B;
     res->n_cols = n_out;
     res->n_layers = nl;

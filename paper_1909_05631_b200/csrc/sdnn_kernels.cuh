@@ -11,24 +11,28 @@
 // B200 formulation
 // ----------------
 // Weights: ELL by output column, inputs ascending, padded to a multiple of
-// 32 slots with index -1.  Every output is ONE sequential chain
+// 32 slots with index -1.  Every (row, output) is ONE sequential chain
 //     acc = ((0 + y[k0]*w0) + y[k1]*w1) + ...      (k0 < k1 < ...)
-// computed by one lane, so float64 reproduces the reference bit for bit
+// kept in one register, so float64 reproduces the reference bit for bit
 // (adding y*w for an unstored y = 0 adds a signed zero, which cannot change
-// a nonzero chain nor make a zero chain nonzero).
+// a nonzero chain nor make a zero chain nonzero -- so zero lines may be
+// skipped or gathered as zeros without changing a bit).
 //
-// Activations: "tiles" of 32 live rows stored neuron-major, one line of
-// 32 values per (tile, neuron): slab[(tile * ld + k) * 32 + lane].  A warp
-// owns an output column j of a tile, lane = row: for each slot it gathers one
-// whole line (128 B in float32) for its 32 rows, so each weight slot loaded
-// serves 32 rows and each gather is a full coalesced line.  A byte mask per
-// (tile, neuron) flags which 32-byte sectors of the line hold a nonzero;
-// zero sectors are neither stored nor loaded (exact: they contribute +-0).
+// Activations: "tiles" of TR live rows (128 in float32, 64 in float64)
+// stored neuron-major: one 512-byte line per (tile, neuron),
+//     slab[(tile * ld + k) * TR + r],
+// lane l of a warp owns rows l*RPL .. l*RPL+RPL-1 (RPL = 16 B / sizeof(T)).
+// A warp computes one output column of a tile: per weight slot it gathers
+// one whole line (every lane one 16-byte load), so one weight slot serves
+// TR rows.  A byte per (tile, neuron) flags which 64-byte groups (4 lanes)
+// of the line hold a nonzero; zero groups are not stored, and their gathers
+// read the tile's dedicated zero line (line ld-1) instead; slots whose whole
+// line is zero are dropped from the warp's slot list before any gather.
 //
-// One cooperative persistent kernel walks all layers: densify Y0 (CSR) into
-// tiles, then per layer a work list of (live tile, output block) items, a
-// grid barrier between layers, and a per-layer live-tile count so layers
-// after the last live row cost a loop iteration.
+// A cooperative persistent kernel walks all layers with one grid barrier per
+// live layer and a per-layer live-tile count, so layers after the last live
+// row cost a loop iteration.  Y0 (CSR) is expanded into tiles by
+// densify_kernel beforehand.
 #pragma once
 
 #include <cstdint>
@@ -65,6 +69,39 @@ __device__ __forceinline__ T bias_relu_clamp_stored(T z, T bias, T ymax) {
     return T(0);
 }
 
+// Tile geometry.
+constexpr int kLineBytes = 512;  // one (tile, neuron) line: 32 lanes x 16 B
+template <typename T>
+__host__ __device__ constexpr int rows_per_lane() { return 16 / (int)sizeof(T); }
+template <typename T>
+__host__ __device__ constexpr int tile_rows() { return 32 * rows_per_lane<T>(); }
+// alive words per (layer, tile): one per lane component, plus an "any" flag
+template <typename T>
+__host__ __device__ constexpr int alive_words() { return rows_per_lane<T>() + 1; }
+
+// 16-byte line piece of one lane <-> its RPL values
+__device__ __forceinline__ void ld16(float (&d)[4], const char* p) {
+    const float4 v = *reinterpret_cast<const float4*>(p);
+    d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+}
+__device__ __forceinline__ void ld16(double (&d)[2], const char* p) {
+    const double2 v = *reinterpret_cast<const double2*>(p);
+    d[0] = v.x; d[1] = v.y;
+}
+__device__ __forceinline__ void st16(char* p, const float (&d)[4]) {
+    *reinterpret_cast<float4*>(p) = make_float4(d[0], d[1], d[2], d[3]);
+}
+__device__ __forceinline__ void st16(char* p, const double (&d)[2]) {
+    *reinterpret_cast<double2*>(p) = make_double2(d[0], d[1]);
+}
+
+// One live slot of a warp's compacted slot list.
+template <typename T>
+struct SlotEntry {
+    unsigned off;  // line byte offset k * 512 | group mask of that line
+    T w;           // weight
+};
+
 template <typename T>
 struct LayerDesc {
     const int32_t* idx;  // [n_out][wp] input index ascending, -1 = padding
@@ -76,20 +113,15 @@ struct LayerDesc {
 template <typename T>
 struct NetArgs {
     int n_in, n_out;      // input lines per tile, outputs per layer
-    int ld;               // per-tile line stride of slabs (>= n_in, n_out)
-    int mstride;          // per-tile byte stride of masks (ld rounded to 16)
+    int ld;               // lines per tile (>= n_in, n_out, plus the zero line)
     int L;
     const LayerDesc<T>* layers;
     T ymax;
     int epilogue;         // 1: bias/ReLU/clamp; 0: raw Z (engine.spmm)
     int n_tiles;
-    const int32_t* rowid; // [n_tiles * 32] batch row of each lane, -1 empty
-    const int64_t* csr_off;
-    const int32_t* csr_cols;
-    const T* csr_vals;
-    T* slab[2];           // [n_tiles][ld][32]
-    uint8_t* mask[2];     // [n_tiles][mstride]
-    uint32_t* alive;      // [L + 1][n_tiles] lane bits of rows with an entry
+    T* slab[2];           // [n_tiles][ld][TR]
+    uint8_t* mask[2];     // [n_tiles][ld] nonzero 64-byte groups of each line
+    uint32_t* alive;      // [L + 1][n_tiles][alive_words] live-row bits
     int32_t* tile_count;  // [L + 1] tiles with any live row
     unsigned* bar;        // grid barrier {count, generation}
     unsigned long long* stamps;  // [L + 1] globaltimer after each layer, or null
@@ -106,6 +138,8 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 
 // Sense-reversing grid barrier for a cooperative launch (all CTAs resident).
+// The gpu-scope fences make every layer's stores visible to the next layer
+// and invalidate this SM's L1, so plain (L1-cached) loads are coherent.
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned n_blocks) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -124,123 +158,156 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned n_blocks) {
     __syncthreads();
 }
 
-__device__ __forceinline__ float ld_cg(const float* p) { return __ldcg(p); }
-__device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
-
-// Rows per 32-byte sector: 8 in float32, 4 in float64.
+// ------------------------------------------------------------ densify
+// Expand Y0 (CSR) into tiles: one block per tile.  Builds the group masks,
+// zeroes every line that will be read, scatters the values, and records
+// the tile's live rows (rows with an entry).
 template <typename T>
-__host__ __device__ constexpr int sector_rows() { return 32 / (int)sizeof(T); }
-
-// ------------------------------------------------------------ phase 0
-// Build tile t of Y0 from CSR: sector masks, zeroed nonzero lines, values.
-template <typename T>
-__device__ void densify_tile(const NetArgs<T>& a, int t, uint32_t* smask_w, uint32_t* s_has) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nw32 = (a.n_in + 3) >> 2;
-    for (int i = tid; i < nw32; i += kThreads) smask_w[i] = 0u;
-    if (tid == 0) *s_has = 0u;
-    __syncthreads();
-    for (int r = warp; r < 32; r += kWarps) {
-        const int row = a.rowid[t * 32 + r];
-        if (row < 0) continue;
-        const uint32_t bit = 1u << (r / sector_rows<T>());
-        const int64_t p0 = a.csr_off[row], p1 = a.csr_off[row + 1];
-        for (int64_t p = p0 + lane; p < p1; p += 32) {
-            const int k = a.csr_cols[p];
-            atomicOr(&smask_w[k >> 2], bit << ((k & 3) * 8));
+__global__ void __launch_bounds__(512) densify_kernel(const int64_t* __restrict__ csr_off,
+                                                      const int32_t* __restrict__ csr_cols,
+                                                      const T* __restrict__ csr_vals,
+                                                      const int32_t* __restrict__ rowid, int n_in, int ld,
+                                                      int n_tiles, T* slab0, T* slab1, uint8_t* mask0,
+                                                      uint32_t* alive0, int32_t* tile_count0) {
+    extern __shared__ __align__(16) uint32_t smask_w[];
+    __shared__ uint32_t s_alive[alive_words<T>()];
+    constexpr int TR = tile_rows<T>(), RPL = rows_per_lane<T>();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        for (int i = tid; i < (n_in + 3) / 4; i += blockDim.x) smask_w[i] = 0u;
+        if (tid < alive_words<T>()) s_alive[tid] = 0u;
+        __syncthreads();
+        for (int r = warp; r < TR; r += nwarp) {
+            const int row = rowid[(size_t)t * TR + r];
+            if (row < 0) continue;
+            const uint32_t bit = 1u << (r / RPL / 4);
+            for (int64_t p = csr_off[row] + lane; p < csr_off[row + 1]; p += 32) {
+                const int k = csr_cols[p];
+                atomicOr(&smask_w[k >> 2], bit << ((k & 3) * 8));
+            }
         }
-    }
-    __syncthreads();
-    const uint8_t* smask = reinterpret_cast<const uint8_t*>(smask_w);
-    uint8_t* gmask = a.mask[0] + (size_t)t * a.mstride;
-    for (int k = tid; k < a.n_in; k += kThreads) gmask[k] = smask[k];
-    // zero every line that will be read (any sector set)
-    T* slab = a.slab[0] + (size_t)t * a.ld * 32;
-    for (int k = warp; k < a.n_in; k += kWarps)
-        if (smask[k]) slab[(size_t)k * 32 + lane] = T(0);
-    __syncthreads();
-    uint32_t has = 0;
-    for (int r = warp; r < 32; r += kWarps) {
-        const int row = a.rowid[t * 32 + r];
-        if (row < 0) continue;
-        const int64_t p0 = a.csr_off[row], p1 = a.csr_off[row + 1];
-        if (p1 > p0) has |= 1u << r;
-        for (int64_t p = p0 + lane; p < p1; p += 32) {
-            const int k = a.csr_cols[p];
-            slab[(size_t)k * 32 + r] = a.csr_vals[p];
+        __syncthreads();
+        const uint8_t* smask = reinterpret_cast<const uint8_t*>(smask_w);
+        uint8_t* gm = mask0 + (size_t)t * ld;
+        for (int k = tid; k < n_in; k += blockDim.x) gm[k] = smask[k];
+        char* s0 = reinterpret_cast<char*>(slab0 + (size_t)t * ld * TR);
+        char* s1 = reinterpret_cast<char*>(slab1 + (size_t)t * ld * TR);
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int k = warp; k < n_in; k += nwarp)
+            if (smask[k]) *reinterpret_cast<float4*>(s0 + (size_t)k * kLineBytes + lane * 16) = z;
+        if (warp == 0) {  // the zero line of both buffers
+            *reinterpret_cast<float4*>(s0 + (size_t)(ld - 1) * kLineBytes + lane * 16) = z;
+            *reinterpret_cast<float4*>(s1 + (size_t)(ld - 1) * kLineBytes + lane * 16) = z;
         }
+        __syncthreads();
+        T* sl = slab0 + (size_t)t * ld * TR;
+        for (int r = warp; r < TR; r += nwarp) {
+            const int row = rowid[(size_t)t * TR + r];
+            if (row < 0) continue;
+            const int64_t p0 = csr_off[row], p1 = csr_off[row + 1];
+            if (lane == 0 && p1 > p0) {
+                atomicOr(&s_alive[r % RPL], 1u << (r / RPL));
+                atomicOr(&s_alive[RPL], 1u);
+            }
+            for (int64_t p = p0 + lane; p < p1; p += 32) sl[(size_t)csr_cols[p] * TR + r] = csr_vals[p];
+        }
+        __syncthreads();
+        if (tid < alive_words<T>()) alive0[(size_t)t * alive_words<T>() + tid] = s_alive[tid];
+        if (tid == 0 && s_alive[RPL]) atomicAdd(tile_count0, 1);
+        __syncthreads();
     }
-    if (lane == 0 && has) atomicOr(s_has, has);
-    __syncthreads();
-    if (tid == 0) {
-        a.alive[t] = *s_has;
-        if (*s_has) atomicAdd(&a.tile_count[0], 1);
-    }
-    __syncthreads();
 }
 
 // ------------------------------------------------------------ one item
-// Output columns [j0, j1) of tile t for layer l: warp per column, lane per row.
+// Output columns [j0, j1) of tile t for layer l: warp per column.
+// Per 32-slot batch, lane s resolves slot s (input line offset, its group
+// mask, weight); slots whose line is entirely zero are dropped and the rest
+// are compacted, in slot order, into the warp's smem list; the list is then
+// gathered 8 lines at a time.  Each lane chains its RPL rows separately.
 template <typename T>
 __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<T>& L, int l, int t,
-                                           int j0, int j1, const uint8_t* smask, uint32_t& alive_acc) {
+                                           int j0, int j1, SlotEntry<T>* wlist, uint32_t (&alive_acc)[4]) {
     using A = Arith<T>;
+    constexpr int RPL = rows_per_lane<T>();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int sec = lane / sector_rows<T>();
-    const T* in = a.slab[l & 1] + (size_t)t * a.ld * 32;
-    T* out = a.slab[(l + 1) & 1] + (size_t)t * a.ld * 32;
-    uint8_t* omask = a.mask[(l + 1) & 1] + (size_t)t * a.mstride;
+    const unsigned gbit = 1u << (lane >> 2);
+    const size_t tile_lines = (size_t)t * a.ld;
+    // select, not index: a runtime index into the parameter struct would
+    // force a local-memory copy of it
+    const bool odd = l & 1;
+    const char* in = reinterpret_cast<const char*>(odd ? a.slab[1] : a.slab[0]) + tile_lines * kLineBytes + lane * 16;
+    char* out = reinterpret_cast<char*>(odd ? a.slab[0] : a.slab[1]) + tile_lines * kLineBytes + lane * 16;
+    const uint8_t* imask = (odd ? a.mask[1] : a.mask[0]) + tile_lines;
+    uint8_t* omask = (odd ? a.mask[0] : a.mask[1]) + tile_lines;
+    const unsigned zoff = (unsigned)(a.ld - 1) * kLineBytes;
     for (int j = j0 + warp; j < j1; j += kWarps) {
-        const int32_t* ip = L.idx + (size_t)j * L.wp;
-        const T* vp = L.val + (size_t)j * L.wp;
-        T acc = T(0);
+        T acc[RPL];
+#pragma unroll
+        for (int c = 0; c < RPL; ++c) acc[c] = T(0);
         for (int s0 = 0; s0 < L.wp; s0 += 32) {
-            const int my_k = __ldg(ip + s0 + lane);
-            const T my_w = __ldg(vp + s0 + lane);
-            T y[32];
-#pragma unroll
-            for (int s = 0; s < 32; ++s) {
-                const int k = __shfl_sync(0xffffffffu, my_k, s);
-                bool live = k >= 0;
-                if (live) live = (smask[k] >> sec) & 1u;
-                y[s] = live ? ld_cg(in + (size_t)k * 32 + lane) : T(0);
+            const int k = __ldg(L.idx + (size_t)j * L.wp + s0 + lane);
+            const T w = __ldg(L.val + (size_t)j * L.wp + s0 + lane);
+            const unsigned m = k >= 0 ? (unsigned)imask[k] : 0u;
+            const unsigned live = __ballot_sync(0xffffffffu, m != 0u);
+            if (m) {
+                SlotEntry<T> e;
+                e.off = (unsigned)k * kLineBytes | m;
+                e.w = w;
+                wlist[__popc(live & ((1u << lane) - 1u))] = e;
             }
+            __syncwarp();
+            const int n = __popc(live);
+            for (int i0 = 0; i0 < n; i0 += 8) {
+                T y[8][RPL];
+                T wv[8];
 #pragma unroll
-            for (int s = 0; s < 32; ++s) {
-                const int k = __shfl_sync(0xffffffffu, my_k, s);
-                const T w = __shfl_sync(0xffffffffu, my_w, s);
-                if (k >= 0) acc = A::add(acc, A::mul(y[s], w));
+                for (int u = 0; u < 8; ++u) {
+                    if (i0 + u < n) {
+                        const SlotEntry<T> e = wlist[i0 + u];
+                        const unsigned off = (e.off & gbit) ? (e.off & ~(unsigned)(kLineBytes - 1)) : zoff;
+                        ld16(y[u], in + off);
+                        wv[u] = e.w;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    if (i0 + u < n) {
+#pragma unroll
+                        for (int c = 0; c < RPL; ++c) acc[c] = A::add(acc[c], A::mul(y[u][c], wv[u]));
+                    }
+                }
             }
+            __syncwarp();
         }
-        const T v = a.epilogue ? bias_relu_clamp(acc, L.bias, a.ymax) : acc;
-        const unsigned nz = __ballot_sync(0xffffffffu, v != T(0));
-        unsigned m = 0;
+        T v[RPL];
+        bool any = false;
 #pragma unroll
-        for (int s = 0; s < 32 / sector_rows<T>(); ++s) {
-            const unsigned rows = ((1u << sector_rows<T>()) - 1u) << (s * sector_rows<T>());
-            if (nz & rows) m |= 1u << s;
+        for (int c = 0; c < RPL; ++c) {
+            v[c] = a.epilogue ? bias_relu_clamp(acc[c], L.bias, a.ymax) : acc[c];
+            any |= v[c] != T(0);
+            alive_acc[c] |= __ballot_sync(0xffffffffu, v[c] != T(0));
         }
-        if ((m >> sec) & 1u) out[(size_t)j * 32 + lane] = v;
-        if (lane == 0) omask[j] = (uint8_t)m;
-        alive_acc |= nz;
+        const unsigned lanes = __ballot_sync(0xffffffffu, any);
+        unsigned om = 0;
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+            if ((lanes >> (4 * g)) & 0xFu) om |= 1u << g;
+        if (om & gbit) st16(out + (size_t)j * kLineBytes, v);
+        if (lane == 0) omask[j] = (uint8_t)om;
     }
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kThreads) net_kernel(NetArgs<T> a) {
+__global__ void __launch_bounds__(kThreads, 2) net_kernel(NetArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem[];
-    // [0, mstride): sector mask of the current tile; then the live-tile list
-    uint8_t* smask = smem;
-    int32_t* tiles = reinterpret_cast<int32_t*>(smem + a.mstride);
+    int32_t* tiles = reinterpret_cast<int32_t*>(smem);
+    __shared__ SlotEntry<T> s_list[kWarps][32];
     __shared__ int s_count;
     __shared__ int s_scan[kWarps + 1];
-    __shared__ uint32_t s_alive;
-    const int tid = threadIdx.x;
+    __shared__ uint32_t s_alive[4];
+    constexpr int RPL = rows_per_lane<T>(), AW = alive_words<T>();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned nb = gridDim.x;
-
-    for (int t = blockIdx.x; t < a.n_tiles; t += gridDim.x)
-        densify_tile<T>(a, t, reinterpret_cast<uint32_t*>(smask), &s_alive);
-    grid_barrier(a.bar, nb);
     if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[0] = globaltimer();
 
     bool all_dead = false;
@@ -248,16 +315,16 @@ __global__ void __launch_bounds__(kThreads) net_kernel(NetArgs<T> a) {
         // zero rows stay zero: once no tile is live every later layer is empty
         if (!all_dead && __ldcg(&a.tile_count[l]) == 0) all_dead = true;
         if (all_dead) continue;
-        const uint32_t* alive_in = a.alive + (size_t)l * a.n_tiles;
-        uint32_t* alive_out = a.alive + (size_t)(l + 1) * a.n_tiles;
+        const uint32_t* alive_in = a.alive + (size_t)l * a.n_tiles * AW;
+        uint32_t* alive_out = a.alive + (size_t)(l + 1) * a.n_tiles * AW;
         // ascending live-tile list (block-wide ordered compaction)
         if (tid == 0) s_count = 0;
         __syncthreads();
         for (int base = 0; base < a.n_tiles; base += kThreads) {
             const int t = base + tid;
-            const bool live = t < a.n_tiles && __ldcg(&alive_in[t]) != 0u;
+            const bool live = t < a.n_tiles && __ldcg(&alive_in[(size_t)t * AW + RPL]) != 0u;
             const unsigned b = __ballot_sync(0xffffffffu, live);
-            if ((tid & 31) == 0) s_scan[tid >> 5] = __popc(b);
+            if (lane == 0) s_scan[warp] = __popc(b);
             __syncthreads();
             if (tid == 0) {
                 int acc = s_count;
@@ -269,7 +336,7 @@ __global__ void __launch_bounds__(kThreads) net_kernel(NetArgs<T> a) {
                 s_scan[kWarps] = acc;
             }
             __syncthreads();
-            if (live) tiles[s_scan[tid >> 5] + __popc(b & ((1u << (tid & 31)) - 1u))] = t;
+            if (live) tiles[s_scan[warp] + __popc(b & ((1u << lane) - 1u))] = t;
             __syncthreads();
             if (tid == 0) s_count = s_scan[kWarps];
             __syncthreads();
@@ -278,29 +345,28 @@ __global__ void __launch_bounds__(kThreads) net_kernel(NetArgs<T> a) {
         const LayerDesc<T> L = a.layers[l];
         const int nblk = (a.n_out + a.jb - 1) / a.jb;
         const long long items = (long long)count * nblk;
-        int cur = -1;
-        if (tid == 0) s_alive = 0u;
+        if (tid < 4) s_alive[tid] = 0u;
+        __syncthreads();
         for (long long it = blockIdx.x; it < items; it += gridDim.x) {
             const int t = tiles[it / nblk];
             const int b = (int)(it % nblk);
-            if (t != cur) {
-                __syncthreads();
-                const int4* src = reinterpret_cast<const int4*>(a.mask[l & 1] + (size_t)t * a.mstride);
-                int4* dst = reinterpret_cast<int4*>(smask);
-                for (int i = tid; i < a.mstride / 16; i += kThreads) dst[i] = __ldcg(src + i);
-                __syncthreads();
-                cur = t;
-            }
-            uint32_t alive_acc = 0;
+            uint32_t alive_acc[4] = {0u, 0u, 0u, 0u};
             const int j0 = b * a.jb, j1 = min(a.n_out, j0 + a.jb);
-            layer_item<T>(a, L, l, t, j0, j1, smask, alive_acc);
-            if ((tid & 31) == 0 && alive_acc) atomicOr(&s_alive, alive_acc);
-            __syncthreads();
-            if (tid == 0 && s_alive) {
-                const uint32_t old = atomicOr(&alive_out[t], s_alive);
-                if (old == 0u) atomicAdd(&a.tile_count[l + 1], 1);
-                s_alive = 0u;
+            layer_item<T>(a, L, l, t, j0, j1, s_list[warp], alive_acc);
+            if (lane == 0) {
+#pragma unroll
+                for (int c = 0; c < RPL; ++c)
+                    if (alive_acc[c]) atomicOr(&s_alive[c], alive_acc[c]);
             }
+            __syncthreads();
+            if (tid < RPL && s_alive[tid]) atomicOr(&alive_out[(size_t)t * AW + tid], s_alive[tid]);
+            if (tid == RPL) {
+                bool any = false;
+                for (int c = 0; c < RPL; ++c) any |= s_alive[c] != 0u;
+                if (any && atomicOr(&alive_out[(size_t)t * AW + RPL], 1u) == 0u) atomicAdd(&a.tile_count[l + 1], 1);
+            }
+            __syncthreads();
+            if (tid < 4) s_alive[tid] = 0u;
             __syncthreads();
         }
         grid_barrier(a.bar, nb);
@@ -308,36 +374,47 @@ __global__ void __launch_bounds__(kThreads) net_kernel(NetArgs<T> a) {
     }
 }
 
-// Read back the rows of each tile of the final slab, one warp per tile, lane
-// per row: pass 1 (pos == null) counts entries, pass 2 writes (column,
-// value) in ascending column order at pos[tile * 32 + lane].
+// Read back the rows of each tile of the final slab, one warp per tile,
+// each lane its RPL rows: pass 1 (pos == null) counts entries, pass 2 writes
+// (column, value) in ascending column order at pos[tile * TR + row].
 template <typename T>
 __global__ void extract_kernel(const T* __restrict__ slab, const uint8_t* __restrict__ mask, int ld,
-                               int mstride, int n_cols, int n_tiles, const int64_t* __restrict__ pos,
+                               int n_cols, int n_tiles, const int64_t* __restrict__ pos,
                                int32_t* __restrict__ counts, int32_t* __restrict__ cols_out,
                                T* __restrict__ vals_out) {
+    constexpr int RPL = rows_per_lane<T>(), TR = tile_rows<T>();
     const int lane = threadIdx.x & 31;
     const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int n_warps = (gridDim.x * blockDim.x) >> 5;
-    const int sec = lane / sector_rows<T>();
+    const unsigned gbit = 1u << (lane >> 2);
     for (int t = warp_global; t < n_tiles; t += n_warps) {
-        const T* s = slab + (size_t)t * ld * 32;
-        const uint8_t* m = mask + (size_t)t * mstride;
-        int64_t at = pos ? pos[t * 32 + lane] : 0;
-        int c = 0;
+        const T* s = slab + (size_t)t * ld * TR + lane * RPL;
+        const uint8_t* m = mask + (size_t)t * ld;
+        int64_t at[RPL];
+        int c[RPL];
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+            at[q] = pos ? pos[(size_t)t * TR + lane * RPL + q] : 0;
+            c[q] = 0;
+        }
         for (int k = 0; k < n_cols; ++k) {
-            if (!((m[k] >> sec) & 1u)) continue;
-            const T v = s[(size_t)k * 32 + lane];
-            if (v != T(0)) {
-                if (pos) {
-                    cols_out[at] = k;
-                    vals_out[at] = v;
-                    ++at;
+            if (!(m[k] & gbit)) continue;
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) {
+                const T v = s[(size_t)k * TR + q];
+                if (v != T(0)) {
+                    if (pos) {
+                        cols_out[at[q]] = k;
+                        vals_out[at[q]] = v;
+                        ++at[q];
+                    }
+                    ++c[q];
                 }
-                ++c;
             }
         }
-        if (!pos) counts[t * 32 + lane] = c;
+        if (!pos)
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) counts[(size_t)t * TR + lane * RPL + q] = c[q];
     }
 }
 
