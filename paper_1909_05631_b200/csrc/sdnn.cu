@@ -108,7 +108,7 @@ struct sdnn_net {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // run scratch, grown on demand
     void* slab[2] = {nullptr, nullptr};
-    uint8_t* mask[2] = {nullptr, nullptr};
+    uint16_t* mask[2] = {nullptr, nullptr};
     int64_t tcap = 0;  // tiles per buffer
     int64_t tcap_lines = 0;
     int32_t* rowid = nullptr;
@@ -233,7 +233,7 @@ int ensure_tiles(sdnn_net* net, int64_t tiles, int64_t ld) {
         const int64_t lines = std::max<int64_t>(tiles, 1) * ld;
         for (int b = 0; b < 2; ++b) {
             CK(cudaMalloc(&net->slab[b], lines * kLineBytes));
-            CK(cudaMalloc(&net->mask[b], lines));
+            CK(cudaMalloc(&net->mask[b], lines * sizeof(uint16_t)));
         }
         net->tcap = tiles;
         net->tcap_lines = lines;
@@ -247,8 +247,8 @@ int64_t wave_rows(sdnn_net* net, int64_t n_rows, int64_t ld, int tr) {
     if (forced > 0) return std::min(forced, std::max<int64_t>(n_rows, 1));
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
-    const int64_t per_tile = 2 * ld * (kLineBytes + 1);
-    int64_t held = net->tcap_lines * (kLineBytes + 1) * 2;
+    const int64_t per_tile = 2 * ld * (kLineBytes + 2);
+    int64_t held = net->tcap_lines * (kLineBytes + 2) * 2;
     int64_t avail = (int64_t)free_b + held - (int64_t)(2ull << 30);
     int64_t w = std::max<int64_t>(1, avail / per_tile) * tr;
     return std::min(w, std::max<int64_t>(n_rows, 1));
@@ -303,7 +303,7 @@ void assemble(sdnn_result* res, std::vector<Piece>& pieces) {
 
 // Final Y of the tiles that are still live -> host CSR pieces.
 template <typename T>
-int extract(sdnn_net* net, const T* slab, const uint8_t* mask, int ld, int n_cols, int64_t n_tiles,
+int extract(sdnn_net* net, const T* slab, const uint16_t* mask, int ld, int n_cols, int64_t n_tiles,
             const std::vector<uint32_t>& alive, const std::vector<int32_t>& rowid, Piece& p) {
     constexpr int TR = tile_rows<T>(), AW = alive_words<T>(), RPL = rows_per_lane<T>();
     p.rows.assign(rowid.begin(), rowid.end());
@@ -447,7 +447,8 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     a.bar = net->bar;
     a.stamps = net->layer_timing ? stamps : nullptr;
     a.jb = env_int("SDNN_JB", net->jb);
-    const size_t dsmem = (size_t)(n_in + 3) / 4 * 4;
+    const int kc = env_int("SDNN_DENSIFY_KC", 192);  // input neurons per staging chunk
+    const size_t dsmem = (size_t)kc * kLineBytes + 2 * TR * sizeof(int64_t);
     const void* dfn = (const void*)densify_kernel<T>;
     CK(cudaFuncSetAttribute(dfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
     const size_t smem = (size_t)tiles1 * 4;
@@ -461,10 +462,10 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     void* args[] = {(void*)&a};
     CK(cudaEventRecord(net->ev0, net->stream));
     if (n_tiles) {
-        const int dgrid = (int)std::min<int64_t>(n_tiles, (int64_t)net->sm_count * 4);
+        const int dgrid = (int)std::min<int64_t>(n_tiles, (int64_t)net->sm_count * 2);
         densify_kernel<T><<<dgrid, 512, dsmem, net->stream>>>(
             batch->off, batch->cols, reinterpret_cast<const T*>(batch->vals), net->rowid, (int)n_in, (int)ld,
-            (int)n_tiles, a.slab[0], a.slab[1], a.mask[0], net->alive, tile_count);
+            (int)n_tiles, kc, a.slab[0], a.slab[1], a.mask[0], net->alive, tile_count);
         CK(cudaGetLastError());
         res->launches += 1;
     }

@@ -24,10 +24,11 @@
 // lane l of a warp owns rows l*RPL .. l*RPL+RPL-1 (RPL = 16 B / sizeof(T)).
 // A warp computes one output column of a tile: per weight slot it gathers
 // one whole line (every lane one 16-byte load), so one weight slot serves
-// TR rows.  A byte per (tile, neuron) flags which 64-byte groups (4 lanes)
-// of the line hold a nonzero; zero groups are not stored, and their gathers
-// read the tile's dedicated zero line (line ld-1) instead; slots whose whole
-// line is zero are dropped from the warp's slot list before any gather.
+// TR rows.  16 bits per (tile, neuron) flag which 32-byte sectors (2 lanes)
+// of the line hold a nonzero; zero sectors are not stored, and their
+// gathers read the tile's dedicated zero line (line ld-1) instead; slots
+// whose whole line is zero are dropped from the warp's slot list before any
+// gather.
 //
 // A cooperative persistent kernel walks all layers with one grid barrier per
 // live layer and a per-layer live-tile count, so layers after the last live
@@ -95,11 +96,12 @@ __device__ __forceinline__ void st16(char* p, const double (&d)[2]) {
     *reinterpret_cast<double2*>(p) = make_double2(d[0], d[1]);
 }
 
-// One live slot of a warp's compacted slot list.
+// One live slot of a warp's compacted slot list (16 bytes).
 template <typename T>
-struct SlotEntry {
-    unsigned off;  // line byte offset k * 512 | group mask of that line
-    T w;           // weight
+struct __align__(16) SlotEntry {
+    unsigned off;   // line byte offset k * 512
+    unsigned mask;  // nonzero sectors of that line
+    T w;            // weight
 };
 
 template <typename T>
@@ -120,7 +122,7 @@ struct NetArgs {
     int epilogue;         // 1: bias/ReLU/clamp; 0: raw Z (engine.spmm)
     int n_tiles;
     T* slab[2];           // [n_tiles][ld][TR]
-    uint8_t* mask[2];     // [n_tiles][ld] nonzero 64-byte groups of each line
+    uint16_t* mask[2];    // [n_tiles][ld] nonzero 32-byte sectors of each line
     uint32_t* alive;      // [L + 1][n_tiles][alive_words] live-row bits
     int32_t* tile_count;  // [L + 1] tiles with any live row
     unsigned* bar;        // grid barrier {count, generation}
@@ -158,60 +160,103 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned n_blocks) {
     __syncthreads();
 }
 
+// Sector mask of a line from the lanes holding a nonzero: bit s <- lanes 2s, 2s+1.
+__device__ __forceinline__ unsigned sector_mask(unsigned lanes) {
+    const unsigned pair = (lanes | (lanes >> 1)) & 0x55555555u;  // bit 2s set if lane 2s or 2s+1
+    // compress even bits to the low 16 bits
+    unsigned x = pair;
+    x = (x | (x >> 1)) & 0x33333333u;
+    x = (x | (x >> 2)) & 0x0F0F0F0Fu;
+    x = (x | (x >> 4)) & 0x00FF00FFu;
+    x = (x | (x >> 8)) & 0x0000FFFFu;
+    return x;
+}
+
 // ------------------------------------------------------------ densify
-// Expand Y0 (CSR) into tiles: one block per tile.  Builds the group masks,
-// zeroes every line that will be read, scatters the values, and records
-// the tile's live rows (rows with an entry).
+// Expand Y0 (CSR) into tiles: one block per tile, KC input neurons at a
+// time.  Each row walks its (ascending) CSR entries with a cursor and drops
+// the chunk's values into a shared [KC][TR] staging tile; the chunk's lines
+// are then written out whole and coalesced (only lines holding a nonzero),
+// with their group masks.  Also records the tile's live rows and zeroes the
+// dedicated zero line of both slab buffers.
 template <typename T>
 __global__ void __launch_bounds__(512) densify_kernel(const int64_t* __restrict__ csr_off,
                                                       const int32_t* __restrict__ csr_cols,
                                                       const T* __restrict__ csr_vals,
                                                       const int32_t* __restrict__ rowid, int n_in, int ld,
-                                                      int n_tiles, T* slab0, T* slab1, uint8_t* mask0,
+                                                      int n_tiles, int kc, T* slab0, T* slab1, uint16_t* mask0,
                                                       uint32_t* alive0, int32_t* tile_count0) {
-    extern __shared__ __align__(16) uint32_t smask_w[];
-    __shared__ uint32_t s_alive[alive_words<T>()];
+    extern __shared__ __align__(16) unsigned char dsm[];
     constexpr int TR = tile_rows<T>(), RPL = rows_per_lane<T>();
+    T* stage = reinterpret_cast<T*>(dsm);                            // [kc][TR]
+    int64_t* cur = reinterpret_cast<int64_t*>(dsm + (size_t)kc * TR * sizeof(T));  // [TR]
+    int64_t* end = cur + TR;
+    __shared__ uint32_t s_alive[alive_words<T>()];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        for (int i = tid; i < (n_in + 3) / 4; i += blockDim.x) smask_w[i] = 0u;
         if (tid < alive_words<T>()) s_alive[tid] = 0u;
         __syncthreads();
-        for (int r = warp; r < TR; r += nwarp) {
+        for (int r = tid; r < TR; r += blockDim.x) {
             const int row = rowid[(size_t)t * TR + r];
-            if (row < 0) continue;
-            const uint32_t bit = 1u << (r / RPL / 4);
-            for (int64_t p = csr_off[row] + lane; p < csr_off[row + 1]; p += 32) {
-                const int k = csr_cols[p];
-                atomicOr(&smask_w[k >> 2], bit << ((k & 3) * 8));
-            }
-        }
-        __syncthreads();
-        const uint8_t* smask = reinterpret_cast<const uint8_t*>(smask_w);
-        uint8_t* gm = mask0 + (size_t)t * ld;
-        for (int k = tid; k < n_in; k += blockDim.x) gm[k] = smask[k];
-        char* s0 = reinterpret_cast<char*>(slab0 + (size_t)t * ld * TR);
-        char* s1 = reinterpret_cast<char*>(slab1 + (size_t)t * ld * TR);
-        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int k = warp; k < n_in; k += nwarp)
-            if (smask[k]) *reinterpret_cast<float4*>(s0 + (size_t)k * kLineBytes + lane * 16) = z;
-        if (warp == 0) {  // the zero line of both buffers
-            *reinterpret_cast<float4*>(s0 + (size_t)(ld - 1) * kLineBytes + lane * 16) = z;
-            *reinterpret_cast<float4*>(s1 + (size_t)(ld - 1) * kLineBytes + lane * 16) = z;
-        }
-        __syncthreads();
-        T* sl = slab0 + (size_t)t * ld * TR;
-        for (int r = warp; r < TR; r += nwarp) {
-            const int row = rowid[(size_t)t * TR + r];
-            if (row < 0) continue;
-            const int64_t p0 = csr_off[row], p1 = csr_off[row + 1];
-            if (lane == 0 && p1 > p0) {
+            cur[r] = row >= 0 ? csr_off[row] : 0;
+            end[r] = row >= 0 ? csr_off[row + 1] : 0;
+            if (row >= 0 && end[r] > cur[r]) {
                 atomicOr(&s_alive[r % RPL], 1u << (r / RPL));
                 atomicOr(&s_alive[RPL], 1u);
             }
-            for (int64_t p = p0 + lane; p < p1; p += 32) sl[(size_t)csr_cols[p] * TR + r] = csr_vals[p];
         }
-        __syncthreads();
+        char* s0 = reinterpret_cast<char*>(slab0 + (size_t)t * ld * TR);
+        char* s1 = reinterpret_cast<char*>(slab1 + (size_t)t * ld * TR);
+        if (warp == 0) {
+            *reinterpret_cast<float4*>(s0 + (size_t)(ld - 1) * kLineBytes + lane * 16) = z;
+            *reinterpret_cast<float4*>(s1 + (size_t)(ld - 1) * kLineBytes + lane * 16) = z;
+        }
+        uint16_t* gm = mask0 + (size_t)t * ld;
+        for (int k0 = 0; k0 < n_in; k0 += kc) {
+            const int kn = min(kc, n_in - k0);
+            float4* st4 = reinterpret_cast<float4*>(stage);
+            for (int i = tid; i < kn * kLineBytes / 16; i += blockDim.x) st4[i] = z;
+            __syncthreads();
+            // each warp advances some rows' cursors through this chunk
+            for (int r = warp; r < TR; r += nwarp) {
+                int64_t p = cur[r];
+                const int64_t e = end[r];
+                while (p < e) {
+                    const int64_t q = p + lane;
+                    const int k = q < e ? csr_cols[q] : INT32_MAX;
+                    const bool in_chunk = k < k0 + kn;
+                    if (in_chunk) stage[(size_t)(k - k0) * TR + r] = csr_vals[q];
+                    const unsigned b = __ballot_sync(0xffffffffu, in_chunk);
+                    const int adv = __popc(b);  // columns ascend: in-chunk lanes are a prefix
+                    p += adv;
+                    if (adv < 32) break;
+                }
+                if (lane == 0) cur[r] = p;
+            }
+            __syncthreads();
+            // write out the chunk's nonzero lines and their group masks
+            for (int k = warp; k < kn; k += nwarp) {
+                T v[RPL];
+                const char* src = reinterpret_cast<const char*>(stage) + (size_t)k * kLineBytes + lane * 16;
+                if (sizeof(T) == 4) {
+                    const float4 q = *reinterpret_cast<const float4*>(src);
+                    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+                } else {
+                    const double2 q = *reinterpret_cast<const double2*>(src);
+                    v[0] = q.x; v[1] = q.y;
+                }
+                bool any = false;
+#pragma unroll
+                for (int c = 0; c < RPL; ++c) any |= v[c] != T(0);
+                const unsigned m = sector_mask(__ballot_sync(0xffffffffu, any));
+                if (m & (1u << (lane >> 1)))
+                    *reinterpret_cast<float4*>(s0 + (size_t)(k0 + k) * kLineBytes + lane * 16) =
+                        *reinterpret_cast<const float4*>(src);
+                if (lane == 0) gm[k0 + k] = (uint16_t)m;
+            }
+            __syncthreads();
+        }
         if (tid < alive_words<T>()) alive0[(size_t)t * alive_words<T>() + tid] = s_alive[tid];
         if (tid == 0 && s_alive[RPL]) atomicAdd(tile_count0, 1);
         __syncthreads();
@@ -220,91 +265,138 @@ __global__ void __launch_bounds__(512) densify_kernel(const int64_t* __restrict_
 
 // ------------------------------------------------------------ one item
 // Output columns [j0, j1) of tile t for layer l: warp per column.
-// Per 32-slot batch, lane s resolves slot s (input line offset, its group
+// The warp walks its columns' 32-slot batches with a three-stage prefetch
+// (slot indices + weights two batches ahead, the lines' group masks one
+// batch ahead).  In a batch, lane s holds slot s (input line offset, group
 // mask, weight); slots whose line is entirely zero are dropped and the rest
-// are compacted, in slot order, into the warp's smem list; the list is then
+// are compacted, in slot order, into the warp's smem list, which is then
 // gathered 8 lines at a time.  Each lane chains its RPL rows separately.
+// Live-row bits go straight to the tile's alive words (one atomic per word).
 template <typename T>
 __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<T>& L, int l, int t,
-                                           int j0, int j1, SlotEntry<T>* wlist, uint32_t (&alive_acc)[4]) {
+                                           int j0, int j1, SlotEntry<T>* wlist) {
     using A = Arith<T>;
-    constexpr int RPL = rows_per_lane<T>();
+    constexpr int RPL = rows_per_lane<T>(), AW = alive_words<T>();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const unsigned gbit = 1u << (lane >> 2);
+    const unsigned sbit = 1u << (lane >> 1);
     const size_t tile_lines = (size_t)t * a.ld;
     // select, not index: a runtime index into the parameter struct would
     // force a local-memory copy of it
     const bool odd = l & 1;
     const char* in = reinterpret_cast<const char*>(odd ? a.slab[1] : a.slab[0]) + tile_lines * kLineBytes + lane * 16;
     char* out = reinterpret_cast<char*>(odd ? a.slab[0] : a.slab[1]) + tile_lines * kLineBytes + lane * 16;
-    const uint8_t* imask = (odd ? a.mask[1] : a.mask[0]) + tile_lines;
-    uint8_t* omask = (odd ? a.mask[0] : a.mask[1]) + tile_lines;
+    const uint16_t* imask = (odd ? a.mask[1] : a.mask[0]) + tile_lines;
+    uint16_t* omask = (odd ? a.mask[0] : a.mask[1]) + tile_lines;
     const unsigned zoff = (unsigned)(a.ld - 1) * kLineBytes;
-    for (int j = j0 + warp; j < j1; j += kWarps) {
-        T acc[RPL];
+    const int jw = j0 + warp;
+    if (jw >= j1) return;
+    const int nb = L.wp / 32;  // batches per column
+    const int n_cols = (j1 - jw + kWarps - 1) / kWarps;
+    const int total = n_cols * nb;
+    if (total == 0) {  // zero-width layer: every output is an empty chain
+        for (int j = jw; j < j1; j += kWarps)
+            if (lane == 0) omask[j] = 0;
+        return;
+    }
+    auto slot_ptr = [&](int b) {
+        const int j = jw + (b / nb) * kWarps;
+        return (size_t)j * L.wp + (size_t)(b % nb) * 32 + lane;
+    };
+    // pipeline registers: (k1, w1) for batch b+1, (k2, w2) for batch b+2
+    int k0 = __ldg(L.idx + slot_ptr(0));
+    T w0 = __ldg(L.val + slot_ptr(0));
+    int k1 = -1, k2 = -1;
+    T w1 = T(0), w2 = T(0);
+    if (total > 1) {
+        k1 = __ldg(L.idx + slot_ptr(1));
+        w1 = __ldg(L.val + slot_ptr(1));
+    }
+    unsigned m0 = k0 >= 0 ? (unsigned)imask[k0] : 0u;
+    T acc[RPL];
+    uint32_t alive_acc[RPL];
 #pragma unroll
-        for (int c = 0; c < RPL; ++c) acc[c] = T(0);
-        for (int s0 = 0; s0 < L.wp; s0 += 32) {
-            const int k = __ldg(L.idx + (size_t)j * L.wp + s0 + lane);
-            const T w = __ldg(L.val + (size_t)j * L.wp + s0 + lane);
-            const unsigned m = k >= 0 ? (unsigned)imask[k] : 0u;
-            const unsigned live = __ballot_sync(0xffffffffu, m != 0u);
-            if (m) {
-                SlotEntry<T> e;
-                e.off = (unsigned)k * kLineBytes | m;
-                e.w = w;
-                wlist[__popc(live & ((1u << lane) - 1u))] = e;
-            }
-            __syncwarp();
-            const int n = __popc(live);
-            for (int i0 = 0; i0 < n; i0 += 8) {
-                T y[8][RPL];
-                T wv[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    if (i0 + u < n) {
-                        const SlotEntry<T> e = wlist[i0 + u];
-                        const unsigned off = (e.off & gbit) ? (e.off & ~(unsigned)(kLineBytes - 1)) : zoff;
-                        ld16(y[u], in + off);
-                        wv[u] = e.w;
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    if (i0 + u < n) {
-#pragma unroll
-                        for (int c = 0; c < RPL; ++c) acc[c] = A::add(acc[c], A::mul(y[u][c], wv[u]));
-                    }
-                }
-            }
-            __syncwarp();
+    for (int c = 0; c < RPL; ++c) {
+        acc[c] = T(0);
+        alive_acc[c] = 0u;
+    }
+    for (int b = 0; b < total; ++b) {
+        // issue the next loads before working on batch b
+        if (b + 2 < total) {
+            k2 = __ldg(L.idx + slot_ptr(b + 2));
+            w2 = __ldg(L.val + slot_ptr(b + 2));
         }
-        T v[RPL];
-        bool any = false;
-#pragma unroll
-        for (int c = 0; c < RPL; ++c) {
-            v[c] = a.epilogue ? bias_relu_clamp(acc[c], L.bias, a.ymax) : acc[c];
-            any |= v[c] != T(0);
-            alive_acc[c] |= __ballot_sync(0xffffffffu, v[c] != T(0));
+        const unsigned m1 = (b + 1 < total && k1 >= 0) ? (unsigned)imask[k1] : 0u;
+
+        const unsigned live = __ballot_sync(0xffffffffu, m0 != 0u);
+        if (m0) {
+            SlotEntry<T> e;
+            e.off = (unsigned)k0 * kLineBytes;
+            e.mask = m0;
+            e.w = w0;
+            wlist[__popc(live & ((1u << lane) - 1u))] = e;
         }
-        const unsigned lanes = __ballot_sync(0xffffffffu, any);
-        unsigned om = 0;
+        __syncwarp();
+        const int n = __popc(live);
+        for (int i0 = 0; i0 < n; i0 += 8) {
+            T y[8][RPL];
 #pragma unroll
-        for (int g = 0; g < 8; ++g)
-            if ((lanes >> (4 * g)) & 0xFu) om |= 1u << g;
-        if (om & gbit) st16(out + (size_t)j * kLineBytes, v);
-        if (lane == 0) omask[j] = (uint8_t)om;
+            for (int u = 0; u < 8; ++u) {
+                if (i0 + u < n) {
+                    const unsigned off = (wlist[i0 + u].mask & sbit) ? wlist[i0 + u].off : zoff;
+                    ld16(y[u], in + off);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (i0 + u < n) {
+                    const T w = wlist[i0 + u].w;
+#pragma unroll
+                    for (int c = 0; c < RPL; ++c) acc[c] = A::add(acc[c], A::mul(y[u][c], w));
+                }
+            }
+        }
+        __syncwarp();
+        if (b % nb == nb - 1) {  // column complete: epilogue
+            const int j = jw + (b / nb) * kWarps;
+            T v[RPL];
+            bool any = false;
+#pragma unroll
+            for (int c = 0; c < RPL; ++c) {
+                v[c] = a.epilogue ? bias_relu_clamp(acc[c], L.bias, a.ymax) : acc[c];
+                any |= v[c] != T(0);
+                alive_acc[c] |= __ballot_sync(0xffffffffu, v[c] != T(0));
+                acc[c] = T(0);
+            }
+            const unsigned om = sector_mask(__ballot_sync(0xffffffffu, any));
+            if (om & sbit) st16(out + (size_t)j * kLineBytes, v);
+            if (lane == 0) omask[j] = (uint16_t)om;
+        }
+        k0 = k1;
+        w0 = w1;
+        m0 = m1;
+        k1 = k2;
+        w1 = w2;
+    }
+    // live rows of this warp's columns -> the tile's alive words
+    bool any_alive = false;
+#pragma unroll
+    for (int c = 0; c < RPL; ++c) any_alive |= alive_acc[c] != 0u;
+    if (lane == 0 && any_alive) {
+        uint32_t* aw = a.alive + ((size_t)(l + 1) * a.n_tiles + t) * AW;
+#pragma unroll
+        for (int c = 0; c < RPL; ++c)
+            if (alive_acc[c]) atomicOr(&aw[c], alive_acc[c]);
+        if (atomicOr(&aw[RPL], 1u) == 0u) atomicAdd(&a.tile_count[l + 1], 1);
     }
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kThreads, 2) net_kernel(NetArgs<T> a) {
+__global__ void __launch_bounds__(kThreads, 3) net_kernel(NetArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem[];
     int32_t* tiles = reinterpret_cast<int32_t*>(smem);
     __shared__ SlotEntry<T> s_list[kWarps][32];
     __shared__ int s_count;
     __shared__ int s_scan[kWarps + 1];
-    __shared__ uint32_t s_alive[4];
     constexpr int RPL = rows_per_lane<T>(), AW = alive_words<T>();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned nb = gridDim.x;
@@ -316,7 +408,6 @@ __global__ void __launch_bounds__(kThreads, 2) net_kernel(NetArgs<T> a) {
         if (!all_dead && __ldcg(&a.tile_count[l]) == 0) all_dead = true;
         if (all_dead) continue;
         const uint32_t* alive_in = a.alive + (size_t)l * a.n_tiles * AW;
-        uint32_t* alive_out = a.alive + (size_t)(l + 1) * a.n_tiles * AW;
         // ascending live-tile list (block-wide ordered compaction)
         if (tid == 0) s_count = 0;
         __syncthreads();
@@ -345,29 +436,11 @@ __global__ void __launch_bounds__(kThreads, 2) net_kernel(NetArgs<T> a) {
         const LayerDesc<T> L = a.layers[l];
         const int nblk = (a.n_out + a.jb - 1) / a.jb;
         const long long items = (long long)count * nblk;
-        if (tid < 4) s_alive[tid] = 0u;
-        __syncthreads();
         for (long long it = blockIdx.x; it < items; it += gridDim.x) {
             const int t = tiles[it / nblk];
             const int b = (int)(it % nblk);
-            uint32_t alive_acc[4] = {0u, 0u, 0u, 0u};
             const int j0 = b * a.jb, j1 = min(a.n_out, j0 + a.jb);
-            layer_item<T>(a, L, l, t, j0, j1, s_list[warp], alive_acc);
-            if (lane == 0) {
-#pragma unroll
-                for (int c = 0; c < RPL; ++c)
-                    if (alive_acc[c]) atomicOr(&s_alive[c], alive_acc[c]);
-            }
-            __syncthreads();
-            if (tid < RPL && s_alive[tid]) atomicOr(&alive_out[(size_t)t * AW + tid], s_alive[tid]);
-            if (tid == RPL) {
-                bool any = false;
-                for (int c = 0; c < RPL; ++c) any |= s_alive[c] != 0u;
-                if (any && atomicOr(&alive_out[(size_t)t * AW + RPL], 1u) == 0u) atomicAdd(&a.tile_count[l + 1], 1);
-            }
-            __syncthreads();
-            if (tid < 4) s_alive[tid] = 0u;
-            __syncthreads();
+            layer_item<T>(a, L, l, t, j0, j1, s_list[warp]);
         }
         grid_barrier(a.bar, nb);
         if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[l + 1] = globaltimer();
@@ -378,7 +451,7 @@ __global__ void __launch_bounds__(kThreads, 2) net_kernel(NetArgs<T> a) {
 // each lane its RPL rows: pass 1 (pos == null) counts entries, pass 2 writes
 // (column, value) in ascending column order at pos[tile * TR + row].
 template <typename T>
-__global__ void extract_kernel(const T* __restrict__ slab, const uint8_t* __restrict__ mask, int ld,
+__global__ void extract_kernel(const T* __restrict__ slab, const uint16_t* __restrict__ mask, int ld,
                                int n_cols, int n_tiles, const int64_t* __restrict__ pos,
                                int32_t* __restrict__ counts, int32_t* __restrict__ cols_out,
                                T* __restrict__ vals_out) {
@@ -386,10 +459,10 @@ __global__ void extract_kernel(const T* __restrict__ slab, const uint8_t* __rest
     const int lane = threadIdx.x & 31;
     const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int n_warps = (gridDim.x * blockDim.x) >> 5;
-    const unsigned gbit = 1u << (lane >> 2);
+    const unsigned sbit = 1u << (lane >> 1);
     for (int t = warp_global; t < n_tiles; t += n_warps) {
         const T* s = slab + (size_t)t * ld * TR + lane * RPL;
-        const uint8_t* m = mask + (size_t)t * ld;
+        const uint16_t* m = mask + (size_t)t * ld;
         int64_t at[RPL];
         int c[RPL];
 #pragma unroll
@@ -398,7 +471,7 @@ __global__ void extract_kernel(const T* __restrict__ slab, const uint8_t* __rest
             c[q] = 0;
         }
         for (int k = 0; k < n_cols; ++k) {
-            if (!(m[k] & gbit)) continue;
+            if (!(m[k] & sbit)) continue;
 #pragma unroll
             for (int q = 0; q < RPL; ++q) {
                 const T v = s[(size_t)k * TR + q];

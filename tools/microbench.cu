@@ -58,6 +58,26 @@ __global__ void l2_word_gather(const float* __restrict__ buf, int n_words, int i
     if (acc == -1.f) out[0] = acc;
 }
 
+// 512-byte line per warp request (16 B per lane), MLP = U lines in flight
+template <int U>
+__global__ void l2_line512_gather(const float4* __restrict__ slab, int n_lines, int iters, float* out) {
+    const int lane = threadIdx.x & 31;
+    uint32_t st = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 2654435761u + 99u;
+    float acc = 0.f;
+    for (int i = 0; i < iters; i += U) {
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            uint32_t r = lcg(st);
+            uint32_t line = (r >> 4) % n_lines;
+            v[u] = slab[(size_t)line * 32 + lane];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc += v[u].x + v[u].y + v[u].z + v[u].w;
+    }
+    if (acc == -1.f) out[0] = acc;
+}
+
 int main() {
     int dev = 0, sms = 0, clk = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -115,6 +135,33 @@ int main() {
         cudaEventElapsedTime(&ms, a, b);
         double words_s = (double)grid * threads * it / (ms * 1e-3);
         printf("L2 word gather %d MB: %.3g words/s (%.2f per SM per ns)\n", mb, words_s, words_s / sms / 1e9);
+        cudaFree(slab);
+    }
+    for (int mb : {32, 96}) {
+        size_t bytes = (size_t)mb << 20;
+        float4* slab;
+        CK(cudaMalloc(&slab, bytes));
+        cudaMemset(slab, 0, bytes);
+        int n_lines = (int)(bytes / 512);
+        for (int occ : {2, 4, 8}) {
+            int grid = sms * occ, threads = 256, it = 1024;
+            float ms;
+            l2_line512_gather<8><<<grid, threads>>>(slab, n_lines, it, out);
+            cudaEventRecord(a);
+            l2_line512_gather<8><<<grid, threads>>>(slab, n_lines, it, out);
+            cudaEventRecord(b);
+            CK(cudaEventSynchronize(b));
+            cudaEventElapsedTime(&ms, a, b);
+            double lines = (double)grid * (threads / 32) * it;
+            printf("L2 512B-line gather %d MB, %d CTA/SM, MLP 8: %.2f TB/s\n", mb, occ, lines * 512 / (ms * 1e-3) / 1e12);
+            l2_line512_gather<16><<<grid, threads>>>(slab, n_lines, it, out);
+            cudaEventRecord(a);
+            l2_line512_gather<16><<<grid, threads>>>(slab, n_lines, it, out);
+            cudaEventRecord(b);
+            CK(cudaEventSynchronize(b));
+            cudaEventElapsedTime(&ms, a, b);
+            printf("L2 512B-line gather %d MB, %d CTA/SM, MLP 16: %.2f TB/s\n", mb, occ, lines * 512 / (ms * 1e-3) / 1e12);
+        }
         cudaFree(slab);
     }
     return 0;
