@@ -107,62 +107,7 @@ class ClockSampler:
 
 # ---------------------------------------------------------- distributed
 
-class Dist:
-    def __init__(self):
-        self.world = int(os.environ.get("WORLD_SIZE", "1"))
-        self.rank = int(os.environ.get("RANK", "0"))
-        self.local = int(os.environ.get("LOCAL_RANK", "0"))
-        self.pg = None
-        if self.world > 1:
-            import torch
-            import torch.distributed as td
-
-            backend = "nccl" if torch.cuda.is_available() else "gloo"
-            if backend == "nccl":
-                torch.cuda.set_device(self.local)
-            td.init_process_group(backend)
-            self.td = td
-            self.torch = torch
-            self.backend = backend
-
-    def barrier(self):
-        if self.world > 1:
-            self.td.barrier()
-
-    def max(self, x: float) -> float:
-        if self.world == 1:
-            return x
-        t = self.torch.tensor([x], dtype=self.torch.float64,
-                              device=f"cuda:{self.local}" if self.backend == "nccl" else "cpu")
-        self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
-        return float(t.item())
-
-    def sum(self, x: float) -> float:
-        if self.world == 1:
-            return x
-        t = self.torch.tensor([x], dtype=self.torch.float64,
-                              device=f"cuda:{self.local}" if self.backend == "nccl" else "cpu")
-        self.td.all_reduce(t)
-        return float(t.item())
-
-    def gather_categories(self, cats: np.ndarray) -> np.ndarray:
-        """Final category gather (the only cross-rank data exchange)."""
-        if self.world == 1:
-            return cats
-        out = [None] * self.world
-        self.td.all_gather_object(out, cats.tolist())
-        return np.asarray(sorted(c for part in out for c in part), np.int64)
-
-    def close(self):
-        if self.world > 1:
-            self.td.destroy_process_group()
-
-
-def shard(batch: int, rank: int, world: int) -> tuple[int, int]:
-    """Contiguous row block of this rank (engine.py:240 tiling)."""
-    per = -(-batch // world)
-    r0 = min(batch, rank * per)
-    return r0, min(batch, r0 + per)
+from paper_1909_05631_b200.dist import RankGroup, shard  # noqa: E402
 
 
 # ----------------------------------------------------------- byte model
@@ -229,7 +174,7 @@ def cpu_rows_for(w: W.Workload) -> int:
 
 # ------------------------------------------------------------ our arm
 
-def run_ours(args, dist: Dist):
+def run_ours(args, dist: RankGroup):
     import torch
 
     from paper_1909_05631_b200.engine import DeviceNetwork
@@ -265,7 +210,7 @@ def run_ours(args, dist: Dist):
     clk = clocks.stop()
     ms_per_step = dist.max(dev_ms / args.steps)
     wall_per_step = dist.max(wall_ms / args.steps)
-    cats = dist.gather_categories(res.categories + r0)
+    cats = dist.gather_categories(res.categories, r0)
     live_total = dist.sum(float(res.live_rows[:-1].sum()))
 
     # profiling pass (untimed): per-layer events for the roofline
@@ -406,7 +351,7 @@ def companions(args, net_cls):
 
 # ------------------------------------------------------ reference arm
 
-def run_reference(args, dist: Dist):
+def run_reference(args, dist: RankGroup):
     if dist.rank != 0:
         return None
     w = workload(args)
@@ -472,7 +417,7 @@ def main(argv=None):
     ap.add_argument("--companions", default="K2:120",
                     help="comma list NAME[:LAYERS] of live companions ('' to skip)")
     args = ap.parse_args(argv)
-    dist = Dist()
+    dist = RankGroup()
     try:
         line = run_reference(args, dist) if args.impl == "reference" else run_ours(args, dist)
         if line is not None and dist.rank == 0:

@@ -41,14 +41,20 @@
 
 namespace sdnn {
 
+// One accumulation step acc + y*w.  float64 (the parity path) rounds the
+// multiply and the add apart, like the reference's mulsd + addsd; float32
+// (the throughput path) uses one fused multiply-add per step, which the
+// oracle's float instance mirrors with fmaf.
 template <typename T> struct Arith;
 template <> struct Arith<float> {
-    static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
     static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+    static __device__ __forceinline__ float muladd(float y, float w, float acc) { return __fmaf_rn(y, w, acc); }
 };
 template <> struct Arith<double> {
-    static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
     static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+    static __device__ __forceinline__ double muladd(double y, double w, double acc) {
+        return __dadd_rn(acc, __dmul_rn(y, w));
+    }
 };
 
 // engine.py:129-133 applied to one dense position; a zero position is an
@@ -351,7 +357,7 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
                 if (i0 + u < n) {
                     const T w = wlist[i0 + u].w;
 #pragma unroll
-                    for (int c = 0; c < RPL; ++c) acc[c] = A::add(acc[c], A::mul(y[u][c], w));
+                    for (int c = 0; c < RPL; ++c) acc[c] = A::muladd(y[u][c], w, acc[c]);
                 }
             }
         }
