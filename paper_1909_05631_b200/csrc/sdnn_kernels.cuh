@@ -95,11 +95,14 @@ __device__ __forceinline__ void ld16(double (&d)[2], const char* p) {
     const double2 v = *reinterpret_cast<const double2*>(p);
     d[0] = v.x; d[1] = v.y;
 }
+// Output lines are streamed (evict-first): a layer's output is read only in
+// the next layer, after the whole slab has been written, so keeping it in L2
+// would only push out the input lines still being gathered.
 __device__ __forceinline__ void st16(char* p, const float (&d)[4]) {
-    *reinterpret_cast<float4*>(p) = make_float4(d[0], d[1], d[2], d[3]);
+    __stcs(reinterpret_cast<float4*>(p), make_float4(d[0], d[1], d[2], d[3]));
 }
 __device__ __forceinline__ void st16(char* p, const double (&d)[2]) {
-    *reinterpret_cast<double2*>(p) = make_double2(d[0], d[1]);
+    __stcs(reinterpret_cast<double2*>(p), make_double2(d[0], d[1]));
 }
 
 // One live slot of a warp's compacted slot list (16 bytes).
@@ -375,7 +378,7 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
             }
             const unsigned om = sector_mask(__ballot_sync(0xffffffffu, any));
             if (om & sbit) st16(out + (size_t)j * kLineBytes, v);
-            if (lane == 0) omask[j] = (uint16_t)om;
+            if (lane == 0) __stcs(reinterpret_cast<unsigned short*>(omask + j), (unsigned short)om);
         }
         k0 = k1;
         w0 = w1;

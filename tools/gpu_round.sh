@@ -1,0 +1,11 @@
+#!/bin/bash
+# Round evidence: default bench line, reference arm, launch list, clocks (run via gpurun)
+mkdir -p gpurun_out
+timeout 1800 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err
+echo "bench exit $?"; tail -c 3000 gpurun_out/bench_default.json
+timeout 1200 python bench.py --impl reference --steps 1 --warmup 1 > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err
+echo "reference exit $?"; cat gpurun_out/bench_reference.json
+timeout 1200 python bench.py --steps 2 --warmup 1 --companions '' --no-cpu > gpurun_out/launch_plain.log 2>&1 && \
+timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+   --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --companions '' --no-cpu > gpurun_out/launch_ncu.log 2>&1
+echo "launch list exit $?"
