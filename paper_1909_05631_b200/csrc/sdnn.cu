@@ -447,12 +447,13 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     a.bar = net->bar;
     a.stamps = net->layer_timing ? stamps : nullptr;
     a.jb = env_int("SDNN_JB", net->jb);
-    const int kc = env_int("SDNN_DENSIFY_KC", 192);  // input neurons per staging chunk
-    const size_t dsmem = (size_t)kc * kLineBytes + 2 * TR * sizeof(int64_t);
+    const int kc = env_int("SDNN_DENSIFY_KC", 96);  // input neurons per staging chunk
+    const size_t dsmem = (size_t)kc * kLineBytes;
     const void* dfn = (const void*)densify_kernel<T>;
     CK(cudaFuncSetAttribute(dfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
     const size_t smem = (size_t)tiles1 * 4;
-    const void* fn = (const void*)net_kernel<T>;
+    const int gb = env_int("SDNN_GB", 8);
+    const void* fn = gb >= 16 ? (const void*)net_kernel<T, 16> : (const void*)net_kernel<T, 8>;
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem));
@@ -462,8 +463,8 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     void* args[] = {(void*)&a};
     CK(cudaEventRecord(net->ev0, net->stream));
     if (n_tiles) {
-        const int dgrid = (int)std::min<int64_t>(n_tiles, (int64_t)net->sm_count * 2);
-        densify_kernel<T><<<dgrid, 512, dsmem, net->stream>>>(
+        const int dgrid = (int)std::min<int64_t>(n_tiles, (int64_t)net->sm_count * 4);
+        densify_kernel<T><<<dgrid, TR, dsmem, net->stream>>>(
             batch->off, batch->cols, reinterpret_cast<const T*>(batch->vals), net->rowid, (int)n_in, (int)ld,
             (int)n_tiles, kc, a.slab[0], a.slab[1], a.mask[0], net->alive, tile_count);
         CK(cudaGetLastError());

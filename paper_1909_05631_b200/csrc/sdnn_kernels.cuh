@@ -182,14 +182,15 @@ __device__ __forceinline__ unsigned sector_mask(unsigned lanes) {
 }
 
 // ------------------------------------------------------------ densify
-// Expand Y0 (CSR) into tiles: one block per tile, KC input neurons at a
-// time.  Each row walks its (ascending) CSR entries with a cursor and drops
-// the chunk's values into a shared [KC][TR] staging tile; the chunk's lines
-// are then written out whole and coalesced (only lines holding a nonzero),
-// with their group masks.  Also records the tile's live rows and zeroes the
-// dedicated zero line of both slab buffers.
+// Expand Y0 (CSR) into tiles: one block per tile, thread r owns row r and
+// walks its (ascending) CSR entries with a private cursor, dropping each
+// chunk of kc input neurons into a shared [kc][TR] staging tile; the chunk's
+// lines are then written out whole and coalesced (only lines holding a
+// nonzero), with their sector masks, and the staging tile is re-zeroed.
+// Also records the tile's live rows and zeroes the tile's zero line in both
+// slab buffers.  blockDim.x == TR.
 template <typename T>
-__global__ void __launch_bounds__(512) densify_kernel(const int64_t* __restrict__ csr_off,
+__global__ void __launch_bounds__(128) densify_kernel(const int64_t* __restrict__ csr_off,
                                                       const int32_t* __restrict__ csr_cols,
                                                       const T* __restrict__ csr_vals,
                                                       const int32_t* __restrict__ rowid, int n_in, int ld,
@@ -197,24 +198,30 @@ __global__ void __launch_bounds__(512) densify_kernel(const int64_t* __restrict_
                                                       uint32_t* alive0, int32_t* tile_count0) {
     extern __shared__ __align__(16) unsigned char dsm[];
     constexpr int TR = tile_rows<T>(), RPL = rows_per_lane<T>();
-    T* stage = reinterpret_cast<T*>(dsm);                            // [kc][TR]
-    int64_t* cur = reinterpret_cast<int64_t*>(dsm + (size_t)kc * TR * sizeof(T));  // [TR]
-    int64_t* end = cur + TR;
+    T* stage = reinterpret_cast<T*>(dsm);  // [kc][TR]
     __shared__ uint32_t s_alive[alive_words<T>()];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    {
+        float4* st4 = reinterpret_cast<float4*>(stage);
+        for (int i = tid; i < kc * kLineBytes / 16; i += blockDim.x) st4[i] = z;
+    }
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         if (tid < alive_words<T>()) s_alive[tid] = 0u;
         __syncthreads();
-        for (int r = tid; r < TR; r += blockDim.x) {
-            const int row = rowid[(size_t)t * TR + r];
-            cur[r] = row >= 0 ? csr_off[row] : 0;
-            end[r] = row >= 0 ? csr_off[row + 1] : 0;
-            if (row >= 0 && end[r] > cur[r]) {
-                atomicOr(&s_alive[r % RPL], 1u << (r / RPL));
-                atomicOr(&s_alive[RPL], 1u);
+        int64_t p = 0, e = 0;
+        if (tid < TR) {
+            const int row = rowid[(size_t)t * TR + tid];
+            if (row >= 0) {
+                p = csr_off[row];
+                e = csr_off[row + 1];
+                if (e > p) {
+                    atomicOr(&s_alive[tid % RPL], 1u << (tid / RPL));
+                    atomicOr(&s_alive[RPL], 1u);
+                }
             }
         }
+        int next = p < e ? csr_cols[p] : INT32_MAX;
         char* s0 = reinterpret_cast<char*>(slab0 + (size_t)t * ld * TR);
         char* s1 = reinterpret_cast<char*>(slab1 + (size_t)t * ld * TR);
         if (warp == 0) {
@@ -224,51 +231,33 @@ __global__ void __launch_bounds__(512) densify_kernel(const int64_t* __restrict_
         uint16_t* gm = mask0 + (size_t)t * ld;
         for (int k0 = 0; k0 < n_in; k0 += kc) {
             const int kn = min(kc, n_in - k0);
-            float4* st4 = reinterpret_cast<float4*>(stage);
-            for (int i = tid; i < kn * kLineBytes / 16; i += blockDim.x) st4[i] = z;
-            __syncthreads();
-            // each warp advances some rows' cursors through this chunk
-            for (int r = warp; r < TR; r += nwarp) {
-                int64_t p = cur[r];
-                const int64_t e = end[r];
-                while (p < e) {
-                    const int64_t q = p + lane;
-                    const int k = q < e ? csr_cols[q] : INT32_MAX;
-                    const bool in_chunk = k < k0 + kn;
-                    if (in_chunk) stage[(size_t)(k - k0) * TR + r] = csr_vals[q];
-                    const unsigned b = __ballot_sync(0xffffffffu, in_chunk);
-                    const int adv = __popc(b);  // columns ascend: in-chunk lanes are a prefix
-                    p += adv;
-                    if (adv < 32) break;
-                }
-                if (lane == 0) cur[r] = p;
+            // drop this row's entries of the chunk into the staging tile
+            const bool any_here = __syncthreads_or(next < k0 + kn);
+            if (!any_here) {  // the whole chunk is zero for every row
+                for (int k = tid; k < kn; k += blockDim.x) gm[k0 + k] = 0;
+                continue;
+            }
+            while (next < k0 + kn) {
+                stage[(size_t)(next - k0) * TR + tid] = csr_vals[p];
+                ++p;
+                next = p < e ? csr_cols[p] : INT32_MAX;
             }
             __syncthreads();
-            // write out the chunk's nonzero lines and their group masks
+            // write out the chunk's nonzero lines and their sector masks
             for (int k = warp; k < kn; k += nwarp) {
-                T v[RPL];
-                const char* src = reinterpret_cast<const char*>(stage) + (size_t)k * kLineBytes + lane * 16;
-                if (sizeof(T) == 4) {
-                    const float4 q = *reinterpret_cast<const float4*>(src);
-                    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
-                } else {
-                    const double2 q = *reinterpret_cast<const double2*>(src);
-                    v[0] = q.x; v[1] = q.y;
-                }
-                bool any = false;
-#pragma unroll
-                for (int c = 0; c < RPL; ++c) any |= v[c] != T(0);
+                char* src = reinterpret_cast<char*>(stage) + (size_t)k * kLineBytes + lane * 16;
+                const float4 q = *reinterpret_cast<const float4*>(src);
+                const bool any = (q.x != 0.f) | (q.y != 0.f) | (q.z != 0.f) | (q.w != 0.f);
                 const unsigned m = sector_mask(__ballot_sync(0xffffffffu, any));
                 if (m & (1u << (lane >> 1)))
-                    *reinterpret_cast<float4*>(s0 + (size_t)(k0 + k) * kLineBytes + lane * 16) =
-                        *reinterpret_cast<const float4*>(src);
+                    *reinterpret_cast<float4*>(s0 + (size_t)(k0 + k) * kLineBytes + lane * 16) = q;
                 if (lane == 0) gm[k0 + k] = (uint16_t)m;
+                *reinterpret_cast<float4*>(src) = z;  // re-zero for the next chunk
             }
-            __syncthreads();
         }
+        __syncthreads();
         if (tid < alive_words<T>()) alive0[(size_t)t * alive_words<T>() + tid] = s_alive[tid];
         if (tid == 0 && s_alive[RPL]) atomicAdd(tile_count0, 1);
-        __syncthreads();
     }
 }
 
@@ -279,9 +268,9 @@ __global__ void __launch_bounds__(512) densify_kernel(const int64_t* __restrict_
 // batch ahead).  In a batch, lane s holds slot s (input line offset, group
 // mask, weight); slots whose line is entirely zero are dropped and the rest
 // are compacted, in slot order, into the warp's smem list, which is then
-// gathered 8 lines at a time.  Each lane chains its RPL rows separately.
+// gathered GB lines at a time.  Each lane chains its RPL rows separately.
 // Live-row bits go straight to the tile's alive words (one atomic per word).
-template <typename T>
+template <typename T, int GB>
 __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<T>& L, int l, int t,
                                            int j0, int j1, SlotEntry<T>* wlist) {
     using A = Arith<T>;
@@ -346,17 +335,17 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
         }
         __syncwarp();
         const int n = __popc(live);
-        for (int i0 = 0; i0 < n; i0 += 8) {
-            T y[8][RPL];
+        for (int i0 = 0; i0 < n; i0 += GB) {
+            T y[GB][RPL];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < GB; ++u) {
                 if (i0 + u < n) {
                     const unsigned off = (wlist[i0 + u].mask & sbit) ? wlist[i0 + u].off : zoff;
                     ld16(y[u], in + off);
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < GB; ++u) {
                 if (i0 + u < n) {
                     const T w = wlist[i0 + u].w;
 #pragma unroll
@@ -399,8 +388,10 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
     }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kThreads, 3) net_kernel(NetArgs<T> a) {
+// GB = lines gathered per batch (loads in flight per warp); fewer CTAs per
+// SM for the deeper batch so its registers fit.
+template <typename T, int GB>
+__global__ void __launch_bounds__(kThreads, GB <= 8 ? 3 : 2) net_kernel(NetArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem[];
     int32_t* tiles = reinterpret_cast<int32_t*>(smem);
     __shared__ SlotEntry<T> s_list[kWarps][32];
@@ -449,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 3) net_kernel(NetArgs<T> a) {
             const int t = tiles[it / nblk];
             const int b = (int)(it % nblk);
             const int j0 = b * a.jb, j1 = min(a.n_out, j0 + a.jb);
-            layer_item<T>(a, L, l, t, j0, j1, s_list[warp]);
+            layer_item<T, GB>(a, L, l, t, j0, j1, s_list[warp]);
         }
         grid_barrier(a.bar, nb);
         if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[l + 1] = globaltimer();

@@ -101,3 +101,28 @@ def layer_csr(w: Workload, layer: int):
     _lib.check_gen(_lib.gen().sdnn_gen_ell_to_csr(w.n, w.n, w.width, _lib.ptr(idx), _lib.ptr(vals),
                                                   _lib.ptr(off), _lib.ptr(cols), _lib.ptr(out)))
     return off, cols, out
+
+
+def layers_csr(w: Workload, first: int = 0, count: int | None = None, threads: int | None = None):
+    """Layers [first, first + count) in CSR-by-input form, generated and
+    transposed by `threads` host threads (for the CPU oracle and tests)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    count = w.layers - first if count is None else count
+    t = threads or _threads()
+    idx = np.zeros((max(count, 1), w.n, w.width), np.int32)
+    if count:
+        _lib.check_gen(_lib.gen().sdnn_gen_permunion_ell_layers(
+            w.weight_seed, first, count, w.n, w.width, t, _lib.ptr(idx)))
+    vals = np.full(w.n * w.width, w.value, np.float64)
+
+    def one(i):
+        off = np.zeros(w.n + 1, np.int64)
+        cols = np.zeros(w.n * w.width, np.int64)
+        out = np.zeros(w.n * w.width, np.float64)
+        _lib.check_gen(_lib.gen().sdnn_gen_ell_to_csr(w.n, w.n, w.width, _lib.ptr(idx[i]), _lib.ptr(vals),
+                                                      _lib.ptr(off), _lib.ptr(cols), _lib.ptr(out)))
+        return off, cols, out
+
+    with ThreadPoolExecutor(max_workers=t) as pool:
+        return list(pool.map(one, range(count)))

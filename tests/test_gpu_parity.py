@@ -253,7 +253,7 @@ def test_c1_as_specified_full_size():
     w = W.CONFIGS["C1"]
     off, cols, vals = W.images(w)
     y0 = O.CSR(w.batch, w.n, off, cols, vals)
-    layers = [O.CSR(w.n, w.n, *W.layer_csr(w, l)) for l in range(w.layers)]
+    layers = [O.CSR(w.n, w.n, *c) for c in W.layers_csr(w)]
     want = O.infer(layers, [w.bias] * w.layers, y0, threads=os.cpu_count() or 8)
     for dtype in ("f32", "f64"):
         net = E.DeviceNetwork(w.n, 0, dtype)
@@ -288,3 +288,52 @@ def test_c4_shape_full_batch_row_sample_consistency():
     want = O.infer(layers, [w.bias] * w.layers, O.CSR(64, w.n, s_off, s_cols, s_vals),
                    precision=32, threads=os.cpu_count() or 8)
     assert O.CSR(64, w.n, *part.y).identical(want)
+
+
+def _oracle_rows(w, rows, precision):
+    """Oracle over the first `rows` rows of workload w (all layers)."""
+    off, cols, vals = W.images(w, n_rows=rows)
+    layers = [O.CSR(w.n, w.n, *c) for c in W.layers_csr(w)]
+    return O.infer(layers, [w.bias] * w.layers, O.CSR(rows, w.n, off, cols, vals), w.ymax,
+                   precision=precision, threads=os.cpu_count() or 8)
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_c2_c3_as_specified_full_batch(name):
+    """C2 (N=4096, L=480) and C3 (N=16384, L=1920) over all 60,000 rows on
+    the GPU; categories and live-row counts checked against the oracle on a
+    3,000-row prefix (rows are independent), f32 and f64."""
+    w = W.CONFIGS[name]
+    off, cols, vals = W.images(w)
+    want64 = _oracle_rows(w, 3000, 64)
+    for dtype in ("f32", "f64"):
+        net = E.DeviceNetwork(w.n, 0, dtype)
+        net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias)
+        full = net.run(net.upload_csr(w.batch, off, cols, vals), w.ymax)
+        assert full.live_rows[0] == np.count_nonzero(np.diff(off))
+        head = net.run(net.upload_csr(3000, off[:3001], cols[:off[3000]], vals[:off[3000]]), w.ymax,
+                       want_y=True)
+        if dtype == "f64":
+            assert O.CSR(3000, w.n, *head.y).identical(want64)
+        assert np.array_equal(head.categories, O.categorize(want64))
+        assert np.array_equal(full.categories[full.categories <= 3000], head.categories)
+        net.close()
+
+
+@pytest.mark.parametrize("batch,p", [(1000, 0.1), (15000, 0.35), (60000, 0.7), (240000, 0.7)])
+def test_c5_sweep_cells(batch, p):
+    """C5 sweep cells (N=65536, L=120): full batch on the GPU, oracle on a
+    400-row prefix; categories and the prefix's final Y must agree."""
+    w = W.CONFIGS["C5"].with_(batch=batch, p=p)
+    off, cols, vals = W.images(w)
+    net = E.DeviceNetwork(w.n, 0, "f32")
+    net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias)
+    full = net.run(net.upload_csr(w.batch, off, cols, vals), w.ymax)
+    assert full.live_rows[0] == np.count_nonzero(np.diff(off))
+    rows = min(400, batch)
+    want = _oracle_rows(w, rows, 32)
+    head = net.run(net.upload_csr(rows, off[:rows + 1], cols[:off[rows]], vals[:off[rows]]), w.ymax,
+                   want_y=True)
+    assert O.CSR(rows, w.n, *head.y).identical(want)
+    assert np.array_equal(full.categories[full.categories <= rows], O.categorize(want))
+    net.close()
