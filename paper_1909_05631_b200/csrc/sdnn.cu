@@ -464,7 +464,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     CK(cudaEventRecord(net->ev0, net->stream));
     if (n_tiles) {
         const int dgrid = (int)std::min<int64_t>(n_tiles, (int64_t)net->sm_count * 4);
-        densify_kernel<T><<<dgrid, TR, dsmem, net->stream>>>(
+        densify_kernel<T><<<dgrid, kDensifyThreads, dsmem, net->stream>>>(
             batch->off, batch->cols, reinterpret_cast<const T*>(batch->vals), net->rowid, (int)n_in, (int)ld,
             (int)n_tiles, kc, a.slab[0], a.slab[1], a.mask[0], net->alive, tile_count);
         CK(cudaGetLastError());

@@ -182,25 +182,32 @@ __device__ __forceinline__ unsigned sector_mask(unsigned lanes) {
 }
 
 // ------------------------------------------------------------ densify
-// Expand Y0 (CSR) into tiles: one block per tile, thread r owns row r and
-// walks its (ascending) CSR entries with a private cursor, dropping each
-// chunk of kc input neurons into a shared [kc][TR] staging tile; the chunk's
-// lines are then written out whole and coalesced (only lines holding a
-// nonzero), with their sector masks, and the staging tile is re-zeroed.
-// Also records the tile's live rows and zeroes the tile's zero line in both
-// slab buffers.  blockDim.x == TR.
+// Expand Y0 (CSR) into tiles: one block (8 warps) per tile; warp w owns rows
+// w, w+8, ...  Each row keeps a 32-entry window of its (ascending) CSR
+// entries in registers, one per lane, and refills it only when every entry
+// of the window is consumed, so a row costs one coalesced load per 32
+// entries however many chunks it spans.  Chunks of kc input neurons are
+// assembled in a shared [kc][TR] staging tile, then written out as whole
+// coalesced lines (only lines holding a nonzero) with their sector masks,
+// and the staging tile is re-zeroed.  Also records the tile's live rows and
+// zeroes the tile's zero line in both slab buffers.
+constexpr int kDensifyThreads = 256;
+
 template <typename T>
-__global__ void __launch_bounds__(128) densify_kernel(const int64_t* __restrict__ csr_off,
-                                                      const int32_t* __restrict__ csr_cols,
-                                                      const T* __restrict__ csr_vals,
-                                                      const int32_t* __restrict__ rowid, int n_in, int ld,
-                                                      int n_tiles, int kc, T* slab0, T* slab1, uint16_t* mask0,
-                                                      uint32_t* alive0, int32_t* tile_count0) {
+__global__ void __launch_bounds__(kDensifyThreads) densify_kernel(const int64_t* __restrict__ csr_off,
+                                                                  const int32_t* __restrict__ csr_cols,
+                                                                  const T* __restrict__ csr_vals,
+                                                                  const int32_t* __restrict__ rowid, int n_in,
+                                                                  int ld, int n_tiles, int kc, T* slab0, T* slab1,
+                                                                  uint16_t* mask0, uint32_t* alive0,
+                                                                  int32_t* tile_count0) {
     extern __shared__ __align__(16) unsigned char dsm[];
     constexpr int TR = tile_rows<T>(), RPL = rows_per_lane<T>();
-    T* stage = reinterpret_cast<T*>(dsm);  // [kc][TR]
+    constexpr int NW = kDensifyThreads / 32, RW = TR / NW;  // rows per warp
+    T* stage = reinterpret_cast<T*>(dsm);                  // [kc][TR]
+    __shared__ int64_t s_pos[TR], s_end[TR];               // window base, row end
     __shared__ uint32_t s_alive[alive_words<T>()];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
     {
         float4* st4 = reinterpret_cast<float4*>(stage);
@@ -209,19 +216,26 @@ __global__ void __launch_bounds__(128) densify_kernel(const int64_t* __restrict_
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         if (tid < alive_words<T>()) s_alive[tid] = 0u;
         __syncthreads();
-        int64_t p = 0, e = 0;
         if (tid < TR) {
             const int row = rowid[(size_t)t * TR + tid];
-            if (row >= 0) {
-                p = csr_off[row];
-                e = csr_off[row + 1];
-                if (e > p) {
-                    atomicOr(&s_alive[tid % RPL], 1u << (tid / RPL));
-                    atomicOr(&s_alive[RPL], 1u);
-                }
+            const int64_t p = row >= 0 ? csr_off[row] : 0, e = row >= 0 ? csr_off[row + 1] : 0;
+            s_pos[tid] = p;
+            s_end[tid] = e;
+            if (e > p) {
+                atomicOr(&s_alive[tid % RPL], 1u << (tid / RPL));
+                atomicOr(&s_alive[RPL], 1u);
             }
         }
-        int next = p < e ? csr_cols[p] : INT32_MAX;
+        __syncthreads();
+        int cb[RW];
+        T vb[RW];
+#pragma unroll
+        for (int i = 0; i < RW; ++i) {
+            const int r = warp + i * NW;
+            const int64_t q = s_pos[r] + lane;
+            cb[i] = q < s_end[r] ? csr_cols[q] : INT32_MAX;
+            vb[i] = q < s_end[r] ? csr_vals[q] : T(0);
+        }
         char* s0 = reinterpret_cast<char*>(slab0 + (size_t)t * ld * TR);
         char* s1 = reinterpret_cast<char*>(slab1 + (size_t)t * ld * TR);
         if (warp == 0) {
@@ -231,20 +245,35 @@ __global__ void __launch_bounds__(128) densify_kernel(const int64_t* __restrict_
         uint16_t* gm = mask0 + (size_t)t * ld;
         for (int k0 = 0; k0 < n_in; k0 += kc) {
             const int kn = min(kc, n_in - k0);
-            // drop this row's entries of the chunk into the staging tile
-            const bool any_here = __syncthreads_or(next < k0 + kn);
-            if (!any_here) {  // the whole chunk is zero for every row
+            bool mine = false;
+#pragma unroll
+            for (int i = 0; i < RW; ++i) mine |= cb[i] < k0 + kn;
+            if (!__syncthreads_or(mine)) {  // the whole chunk is zero for every row
                 for (int k = tid; k < kn; k += blockDim.x) gm[k0 + k] = 0;
                 continue;
             }
-            while (next < k0 + kn) {
-                stage[(size_t)(next - k0) * TR + tid] = csr_vals[p];
-                ++p;
-                next = p < e ? csr_cols[p] : INT32_MAX;
+#pragma unroll
+            for (int i = 0; i < RW; ++i) {
+                const int r = warp + i * NW;
+                while (true) {
+                    if (cb[i] < k0 + kn) {
+                        stage[(size_t)(cb[i] - k0) * TR + r] = vb[i];
+                        cb[i] = INT32_MAX;
+                    }
+                    if (__ballot_sync(0xffffffffu, cb[i] != INT32_MAX)) break;  // window not used up
+                    const int64_t base = s_pos[r] + 32;
+                    if (base >= s_end[r]) break;                              // row done
+                    __syncwarp();  // every lane has read s_pos[r]
+                    if (lane == 0) s_pos[r] = base;
+                    __syncwarp();  // the new base is visible to later reads
+                    const int64_t q = base + lane;
+                    cb[i] = q < s_end[r] ? csr_cols[q] : INT32_MAX;
+                    vb[i] = q < s_end[r] ? csr_vals[q] : T(0);
+                }
             }
             __syncthreads();
             // write out the chunk's nonzero lines and their sector masks
-            for (int k = warp; k < kn; k += nwarp) {
+            for (int k = warp; k < kn; k += NW) {
                 char* src = reinterpret_cast<char*>(stage) + (size_t)k * kLineBytes + lane * 16;
                 const float4 q = *reinterpret_cast<const float4*>(src);
                 const bool any = (q.x != 0.f) | (q.y != 0.f) | (q.z != 0.f) | (q.w != 0.f);

@@ -1,0 +1,8 @@
+#!/bin/bash
+# ncu capture of one kernel (KREGEX) on reduced C4 (run via gpurun)
+ARGS="--workload C4 --batch ${PROF_BATCH:-6000} --layers ${PROF_LAYERS:-3} --steps 1 --warmup 1 --companions '' --no-cpu"
+TAG=${TAG:-prof}
+eval timeout 600 python bench.py $ARGS > gpurun_out/${TAG}_plain.log 2>&1 && \
+eval timeout 1500 ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-net_kernel} -s 1 -c 1 \
+    -o gpurun_out/${TAG} python bench.py $ARGS > gpurun_out/${TAG}_ncu.log 2>&1
+echo "exit $?"
