@@ -108,7 +108,7 @@ struct sdnn_net {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // run scratch, grown on demand
     void* slab[2] = {nullptr, nullptr};
-    uint16_t* mask[2] = {nullptr, nullptr};
+    uint32_t* mask[2] = {nullptr, nullptr};
     int64_t tcap = 0;  // tiles per buffer
     int64_t tcap_lines = 0;
     int32_t* rowid = nullptr;
@@ -233,7 +233,7 @@ int ensure_tiles(sdnn_net* net, int64_t tiles, int64_t ld) {
         const int64_t lines = std::max<int64_t>(tiles, 1) * ld;
         for (int b = 0; b < 2; ++b) {
             CK(cudaMalloc(&net->slab[b], lines * kLineBytes));
-            CK(cudaMalloc(&net->mask[b], lines * sizeof(uint16_t)));
+            CK(cudaMalloc(&net->mask[b], lines * sizeof(uint32_t)));
         }
         net->tcap = tiles;
         net->tcap_lines = lines;
@@ -247,8 +247,8 @@ int64_t wave_rows(sdnn_net* net, int64_t n_rows, int64_t ld, int tr) {
     if (forced > 0) return std::min(forced, std::max<int64_t>(n_rows, 1));
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
-    const int64_t per_tile = 2 * ld * (kLineBytes + 2);
-    int64_t held = net->tcap_lines * (kLineBytes + 2) * 2;
+    const int64_t per_tile = 2 * ld * (kLineBytes + 4);
+    int64_t held = net->tcap_lines * (kLineBytes + 4) * 2;
     int64_t avail = (int64_t)free_b + held - (int64_t)(2ull << 30);
     int64_t w = std::max<int64_t>(1, avail / per_tile) * tr;
     return std::min(w, std::max<int64_t>(n_rows, 1));
@@ -303,7 +303,7 @@ void assemble(sdnn_result* res, std::vector<Piece>& pieces) {
 
 // Final Y of the tiles that are still live -> host CSR pieces.
 template <typename T>
-int extract(sdnn_net* net, const T* slab, const uint16_t* mask, int ld, int n_cols, int64_t n_tiles,
+int extract(sdnn_net* net, const T* slab, const uint32_t* mask, int ld, int n_cols, int64_t n_tiles,
             const std::vector<uint32_t>& alive, const std::vector<int32_t>& rowid, Piece& p) {
     constexpr int TR = tile_rows<T>(), AW = alive_words<T>(), RPL = rows_per_lane<T>();
     p.rows.assign(rowid.begin(), rowid.end());
@@ -328,7 +328,7 @@ int extract(sdnn_net* net, const T* slab, const uint16_t* mask, int ld, int n_co
         const int64_t t = i / TR;
         const int r = (int)(i % TR);
         // a row counts only if it is live at the end; dead tiles hold stale data
-        const bool live = (alive[t * AW + r % RPL] >> (r / RPL)) & 1u;
+        const bool live = (alive[t * AW + r / 32] >> (r % 32)) & 1u;
         const int64_t c = (live && rowid[i] >= 0) ? cnt[i] : 0;
         at[i] = total;
         p.nnz[i] = c;
@@ -341,7 +341,7 @@ int extract(sdnn_net* net, const T* slab, const uint16_t* mask, int ld, int n_co
     // write pass over runs of consecutive live tiles only
     std::vector<int32_t> live_ids;
     for (int64_t t = 0; t < n_tiles; ++t)
-        if (alive[t * AW + RPL]) live_ids.push_back((int32_t)t);
+        if (alive[t * AW + AW - 1]) live_ids.push_back((int32_t)t);
     for (size_t i = 0; i < live_ids.size();) {
         size_t j = i;
         while (j + 1 < live_ids.size() && live_ids[j + 1] == live_ids[j] + 1) ++j;
@@ -447,13 +447,17 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     a.bar = net->bar;
     a.stamps = net->layer_timing ? stamps : nullptr;
     a.jb = env_int("SDNN_JB", net->jb);
-    const int kc = env_int("SDNN_DENSIFY_KC", 96);  // input neurons per staging chunk
+    const int kc = env_int("SDNN_DENSIFY_KC", 48);  // input neurons per staging chunk
     const size_t dsmem = (size_t)kc * kLineBytes;
     const void* dfn = (const void*)densify_kernel<T>;
     CK(cudaFuncSetAttribute(dfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
     const size_t smem = (size_t)tiles1 * 4;
-    const int gb = env_int("SDNN_GB", 8);
-    const void* fn = gb >= 16 ? (const void*)net_kernel<T, 16> : (const void*)net_kernel<T, 8>;
+    // gather pipeline (lines per sub-batch, double-buffered):
+    // 1 = (4, yes) default, 2 = (2, yes), 3 = (4, no)
+    const int kvar = env_int("SDNN_KVAR", 1);
+    const void* fn = kvar == 2   ? (const void*)net_kernel<T, 2, true>
+                     : kvar == 3 ? (const void*)net_kernel<T, 4, false>
+                                 : (const void*)net_kernel<T, 4, true>;
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem));
@@ -494,7 +498,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
             if (st[l + 1] && st[l]) res->layer_ms[l] += (double)(st[l + 1] - st[l]) * 1e-6;
     for (int64_t t = 0; t < n_tiles; ++t)
         for (int r = 0; r < TR; ++r)
-            if ((alive_last[t * AW + r % RPL] >> (r / RPL)) & 1u) final_rows.push_back(rowid[t * TR + r]);
+            if ((alive_last[t * AW + r / 32] >> (r % 32)) & 1u) final_rows.push_back(rowid[t * TR + r]);
     if (want_y) {
         Piece p;
         const int last = (int)(nl & 1);  // layer nl-1 wrote buffer nl & 1

@@ -13,22 +13,24 @@
 // Weights: ELL by output column, inputs ascending, padded to a multiple of
 // 32 slots with index -1.  Every (row, output) is ONE sequential chain
 //     acc = ((0 + y[k0]*w0) + y[k1]*w1) + ...      (k0 < k1 < ...)
-// kept in one register, so float64 reproduces the reference bit for bit
-// (adding y*w for an unstored y = 0 adds a signed zero, which cannot change
-// a nonzero chain nor make a zero chain nonzero -- so zero lines may be
-// skipped or gathered as zeros without changing a bit).
+// kept in one register, so float64 reproduces the reference bit for bit.
+// Adding y*w for an unstored y = 0 (or a padding weight 0) adds a signed
+// zero; the chain starts at +0 and round-to-nearest never produces -0 from
+// a sum unless both addends are -0, so the chain is never -0 and adding +-0
+// never changes it: zero lines may be skipped or gathered as zeros without
+// changing a bit.
 //
-// Activations: "tiles" of TR live rows (128 in float32, 64 in float64)
-// stored neuron-major: one 512-byte line per (tile, neuron),
+// Activations: "tiles" of TR live rows (256 in float32, 128 in float64)
+// stored neuron-major: one 1 KB line per (tile, neuron),
 //     slab[(tile * ld + k) * TR + r],
-// lane l of a warp owns rows l*RPL .. l*RPL+RPL-1 (RPL = 16 B / sizeof(T)).
-// A warp computes one output column of a tile: per weight slot it gathers
-// one whole line (every lane one 16-byte load), so one weight slot serves
-// TR rows.  16 bits per (tile, neuron) flag which 32-byte sectors (2 lanes)
-// of the line hold a nonzero; zero sectors are not stored, and their
-// gathers read the tile's dedicated zero line (line ld-1) instead; slots
-// whose whole line is zero are dropped from the warp's slot list before any
-// gather.
+// lane l of a warp owns rows l*RPL .. l*RPL+RPL-1 (RPL = 32 B / sizeof(T)),
+// i.e. exactly one 32-byte sector, read with one 256-bit load.  A warp
+// computes one output column of a tile: per weight slot it gathers one whole
+// line, so one weight slot serves TR rows.  A 32-bit mask per (tile, neuron)
+// flags which lanes' sectors hold a nonzero; zero sectors are not stored,
+// and their gathers read the tile's dedicated zero line (line ld-1) instead;
+// slots whose whole line is zero are dropped from the warp's slot list
+// before any gather.
 //
 // A cooperative persistent kernel walks all layers with one grid barrier per
 // live layer and a per-layer live-tile count, so layers after the last live
@@ -77,39 +79,48 @@ __device__ __forceinline__ T bias_relu_clamp_stored(T z, T bias, T ymax) {
 }
 
 // Tile geometry.
-constexpr int kLineBytes = 512;  // one (tile, neuron) line: 32 lanes x 16 B
+constexpr int kLineBytes = 1024;  // one (tile, neuron) line: 32 lanes x 32 B
 template <typename T>
-__host__ __device__ constexpr int rows_per_lane() { return 16 / (int)sizeof(T); }
+__host__ __device__ constexpr int rows_per_lane() { return 32 / (int)sizeof(T); }
 template <typename T>
 __host__ __device__ constexpr int tile_rows() { return 32 * rows_per_lane<T>(); }
-// alive words per (layer, tile): one per lane component, plus an "any" flag
+// live-row bitmap words per (layer, tile), plus an "any row live" flag word
 template <typename T>
-__host__ __device__ constexpr int alive_words() { return rows_per_lane<T>() + 1; }
+__host__ __device__ constexpr int alive_words() { return tile_rows<T>() / 32 + 1; }
 
-// 16-byte line piece of one lane <-> its RPL values
-__device__ __forceinline__ void ld16(float (&d)[4], const char* p) {
-    const float4 v = *reinterpret_cast<const float4*>(p);
-    d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+// One lane's 32-byte sector <-> its RPL values (256-bit accesses).
+__device__ __forceinline__ void ld32(float (&d)[8], const char* p) {
+    asm("ld.global.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3]), "=f"(d[4]), "=f"(d[5]), "=f"(d[6]), "=f"(d[7])
+        : "l"(p));
 }
-__device__ __forceinline__ void ld16(double (&d)[2], const char* p) {
-    const double2 v = *reinterpret_cast<const double2*>(p);
-    d[0] = v.x; d[1] = v.y;
+__device__ __forceinline__ void ld32(double (&d)[4], const char* p) {
+    asm("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(d[0]), "=d"(d[1]), "=d"(d[2]), "=d"(d[3]) : "l"(p));
 }
 // Output lines are streamed (evict-first): a layer's output is read only in
 // the next layer, after the whole slab has been written, so keeping it in L2
 // would only push out the input lines still being gathered.
-__device__ __forceinline__ void st16(char* p, const float (&d)[4]) {
-    __stcs(reinterpret_cast<float4*>(p), make_float4(d[0], d[1], d[2], d[3]));
+__device__ __forceinline__ void st32(char* p, const float (&d)[8]) {
+    asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(d[0]), "f"(d[1]),
+                 "f"(d[2]), "f"(d[3]), "f"(d[4]), "f"(d[5]), "f"(d[6]), "f"(d[7])
+                 : "memory");
 }
-__device__ __forceinline__ void st16(char* p, const double (&d)[2]) {
-    __stcs(reinterpret_cast<double2*>(p), make_double2(d[0], d[1]));
+__device__ __forceinline__ void st32(char* p, const double (&d)[4]) {
+    asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(d[0]), "d"(d[1]), "d"(d[2]), "d"(d[3])
+                 : "memory");
+}
+// Plain (write-back) 32-byte store of raw bits, used by densify.
+__device__ __forceinline__ void st32_bits(char* p, const uint4& a, const uint4& b) {
+    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),
+                 "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+                 : "memory");
 }
 
 // One live slot of a warp's compacted slot list (16 bytes).
 template <typename T>
 struct __align__(16) SlotEntry {
-    unsigned off;   // line byte offset k * 512
-    unsigned mask;  // nonzero sectors of that line
+    unsigned off;   // line byte offset k * 1024
+    unsigned mask;  // lanes whose sector of that line holds a nonzero
     T w;            // weight
 };
 
@@ -131,8 +142,8 @@ struct NetArgs {
     int epilogue;         // 1: bias/ReLU/clamp; 0: raw Z (engine.spmm)
     int n_tiles;
     T* slab[2];           // [n_tiles][ld][TR]
-    uint16_t* mask[2];    // [n_tiles][ld] nonzero 32-byte sectors of each line
-    uint32_t* alive;      // [L + 1][n_tiles][alive_words] live-row bits
+    uint32_t* mask[2];    // [n_tiles][ld] lanes whose sector is nonzero
+    uint32_t* alive;      // [L + 1][n_tiles][alive_words] live-row bitmap + flag
     int32_t* tile_count;  // [L + 1] tiles with any live row
     unsigned* bar;        // grid barrier {count, generation}
     unsigned long long* stamps;  // [L + 1] globaltimer after each layer, or null
@@ -169,16 +180,20 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned n_blocks) {
     __syncthreads();
 }
 
-// Sector mask of a line from the lanes holding a nonzero: bit s <- lanes 2s, 2s+1.
-__device__ __forceinline__ unsigned sector_mask(unsigned lanes) {
-    const unsigned pair = (lanes | (lanes >> 1)) & 0x55555555u;  // bit 2s set if lane 2s or 2s+1
-    // compress even bits to the low 16 bits
-    unsigned x = pair;
-    x = (x | (x >> 1)) & 0x33333333u;
-    x = (x | (x >> 2)) & 0x0F0F0F0Fu;
-    x = (x | (x >> 4)) & 0x00FF00FFu;
-    x = (x | (x >> 8)) & 0x0000FFFFu;
-    return x;
+// Add a lane's RPL live-row bits (bit c = row lane*RPL + c) into the tile's
+// row bitmap: lanes sharing a 32-bit word combine by shuffle, one atomic per
+// word; the tile's flag word records "any row live" and bumps the layer's
+// live-tile count exactly once.
+template <typename T>
+__device__ __forceinline__ void publish_alive(uint32_t* aw, unsigned bits, int32_t* tile_count) {
+    constexpr int RPL = rows_per_lane<T>(), LPW = 32 / RPL;  // lanes per word
+    const int lane = threadIdx.x & 31;
+    unsigned v = bits << ((lane % LPW) * RPL);
+#pragma unroll
+    for (int o = 1; o < LPW; o <<= 1) v |= __shfl_xor_sync(0xffffffffu, v, o);
+    const bool any = __any_sync(0xffffffffu, bits != 0u);
+    if (lane % LPW == 0 && v) atomicOr(&aw[lane / LPW], v);
+    if (lane == 0 && any && atomicOr(&aw[tile_rows<T>() / 32], 1u) == 0u) atomicAdd(tile_count, 1);
 }
 
 // ------------------------------------------------------------ densify
@@ -191,7 +206,7 @@ __device__ __forceinline__ unsigned sector_mask(unsigned lanes) {
 // coalesced lines (only lines holding a nonzero) with their sector masks,
 // and the staging tile is re-zeroed.  Also records the tile's live rows and
 // zeroes the tile's zero line in both slab buffers.
-constexpr int kDensifyThreads = 256;
+constexpr int kDensifyThreads = 512;
 
 template <typename T>
 __global__ void __launch_bounds__(kDensifyThreads) densify_kernel(const int64_t* __restrict__ csr_off,
@@ -199,31 +214,31 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_kernel(const int64_t*
                                                                   const T* __restrict__ csr_vals,
                                                                   const int32_t* __restrict__ rowid, int n_in,
                                                                   int ld, int n_tiles, int kc, T* slab0, T* slab1,
-                                                                  uint16_t* mask0, uint32_t* alive0,
+                                                                  uint32_t* mask0, uint32_t* alive0,
                                                                   int32_t* tile_count0) {
     extern __shared__ __align__(16) unsigned char dsm[];
-    constexpr int TR = tile_rows<T>(), RPL = rows_per_lane<T>();
+    constexpr int TR = tile_rows<T>(), AW = alive_words<T>();
     constexpr int NW = kDensifyThreads / 32, RW = TR / NW;  // rows per warp
     T* stage = reinterpret_cast<T*>(dsm);                  // [kc][TR]
     __shared__ int64_t s_pos[TR], s_end[TR];               // window base, row end
-    __shared__ uint32_t s_alive[alive_words<T>()];
+    __shared__ uint32_t s_alive[AW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
     {
-        float4* st4 = reinterpret_cast<float4*>(stage);
-        for (int i = tid; i < kc * kLineBytes / 16; i += blockDim.x) st4[i] = z;
+        uint4* st4 = reinterpret_cast<uint4*>(stage);
+        for (int i = tid; i < kc * kLineBytes / 16; i += blockDim.x) st4[i] = z4;
     }
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        if (tid < alive_words<T>()) s_alive[tid] = 0u;
+        if (tid < AW) s_alive[tid] = 0u;
         __syncthreads();
-        if (tid < TR) {
-            const int row = rowid[(size_t)t * TR + tid];
+        for (int r = tid; r < TR; r += blockDim.x) {
+            const int row = rowid[(size_t)t * TR + r];
             const int64_t p = row >= 0 ? csr_off[row] : 0, e = row >= 0 ? csr_off[row + 1] : 0;
-            s_pos[tid] = p;
-            s_end[tid] = e;
+            s_pos[r] = p;
+            s_end[r] = e;
             if (e > p) {
-                atomicOr(&s_alive[tid % RPL], 1u << (tid / RPL));
-                atomicOr(&s_alive[RPL], 1u);
+                atomicOr(&s_alive[r / 32], 1u << (r % 32));
+                atomicOr(&s_alive[AW - 1], 1u);
             }
         }
         __syncthreads();
@@ -239,17 +254,17 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_kernel(const int64_t*
         char* s0 = reinterpret_cast<char*>(slab0 + (size_t)t * ld * TR);
         char* s1 = reinterpret_cast<char*>(slab1 + (size_t)t * ld * TR);
         if (warp == 0) {
-            *reinterpret_cast<float4*>(s0 + (size_t)(ld - 1) * kLineBytes + lane * 16) = z;
-            *reinterpret_cast<float4*>(s1 + (size_t)(ld - 1) * kLineBytes + lane * 16) = z;
+            st32_bits(s0 + (size_t)(ld - 1) * kLineBytes + lane * 32, z4, z4);
+            st32_bits(s1 + (size_t)(ld - 1) * kLineBytes + lane * 32, z4, z4);
         }
-        uint16_t* gm = mask0 + (size_t)t * ld;
+        uint32_t* gm = mask0 + (size_t)t * ld;
         for (int k0 = 0; k0 < n_in; k0 += kc) {
             const int kn = min(kc, n_in - k0);
             bool mine = false;
 #pragma unroll
             for (int i = 0; i < RW; ++i) mine |= cb[i] < k0 + kn;
             if (!__syncthreads_or(mine)) {  // the whole chunk is zero for every row
-                for (int k = tid; k < kn; k += blockDim.x) gm[k0 + k] = 0;
+                for (int k = tid; k < kn; k += blockDim.x) gm[k0 + k] = 0u;
                 continue;
             }
 #pragma unroll
@@ -274,46 +289,50 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_kernel(const int64_t*
             __syncthreads();
             // write out the chunk's nonzero lines and their sector masks
             for (int k = warp; k < kn; k += NW) {
-                char* src = reinterpret_cast<char*>(stage) + (size_t)k * kLineBytes + lane * 16;
-                const float4 q = *reinterpret_cast<const float4*>(src);
-                const bool any = (q.x != 0.f) | (q.y != 0.f) | (q.z != 0.f) | (q.w != 0.f);
-                const unsigned m = sector_mask(__ballot_sync(0xffffffffu, any));
-                if (m & (1u << (lane >> 1)))
-                    *reinterpret_cast<float4*>(s0 + (size_t)(k0 + k) * kLineBytes + lane * 16) = q;
-                if (lane == 0) gm[k0 + k] = (uint16_t)m;
-                *reinterpret_cast<float4*>(src) = z;  // re-zero for the next chunk
+                uint4* src = reinterpret_cast<uint4*>(reinterpret_cast<char*>(stage) + (size_t)k * kLineBytes + lane * 32);
+                const uint4 a = src[0], b = src[1];
+                const T* sv = reinterpret_cast<const T*>(src);
+                bool any = false;
+#pragma unroll
+                for (int c = 0; c < rows_per_lane<T>(); ++c) any |= sv[c] != T(0);
+                const unsigned m = __ballot_sync(0xffffffffu, any);
+                if (any) st32_bits(s0 + (size_t)(k0 + k) * kLineBytes + lane * 32, a, b);
+                if (lane == 0) gm[k0 + k] = m;
+                src[0] = z4;  // re-zero for the next chunk
+                src[1] = z4;
             }
         }
         __syncthreads();
-        if (tid < alive_words<T>()) alive0[(size_t)t * alive_words<T>() + tid] = s_alive[tid];
-        if (tid == 0 && s_alive[RPL]) atomicAdd(tile_count0, 1);
+        if (tid < AW) alive0[(size_t)t * AW + tid] = s_alive[tid];
+        if (tid == 0 && s_alive[AW - 1]) atomicAdd(tile_count0, 1);
     }
 }
 
 // ------------------------------------------------------------ one item
 // Output columns [j0, j1) of tile t for layer l: warp per column.
 // The warp walks its columns' 32-slot batches with a three-stage prefetch
-// (slot indices + weights two batches ahead, the lines' group masks one
-// batch ahead).  In a batch, lane s holds slot s (input line offset, group
+// (slot indices + weights two batches ahead, the lines' sector masks one
+// batch ahead).  In a batch, lane s holds slot s (input line offset, sector
 // mask, weight); slots whose line is entirely zero are dropped and the rest
-// are compacted, in slot order, into the warp's smem list, which is then
-// gathered GB lines at a time.  Each lane chains its RPL rows separately.
-// Live-row bits go straight to the tile's alive words (one atomic per word).
-template <typename T, int GB>
+// are compacted, in slot order, into the warp's smem list (padded to a
+// multiple of GB with zero-line, zero-weight entries), which is then
+// gathered GB lines at a time, double-buffered when DBUF.  Each lane chains
+// its RPL rows separately; one 256-bit load per lane per line.
+template <typename T, int GB, bool DBUF>
 __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<T>& L, int l, int t,
                                            int j0, int j1, SlotEntry<T>* wlist) {
     using A = Arith<T>;
     constexpr int RPL = rows_per_lane<T>(), AW = alive_words<T>();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const unsigned sbit = 1u << (lane >> 1);
+    const unsigned lbit = 1u << lane;
     const size_t tile_lines = (size_t)t * a.ld;
     // select, not index: a runtime index into the parameter struct would
     // force a local-memory copy of it
     const bool odd = l & 1;
-    const char* in = reinterpret_cast<const char*>(odd ? a.slab[1] : a.slab[0]) + tile_lines * kLineBytes + lane * 16;
-    char* out = reinterpret_cast<char*>(odd ? a.slab[0] : a.slab[1]) + tile_lines * kLineBytes + lane * 16;
-    const uint16_t* imask = (odd ? a.mask[1] : a.mask[0]) + tile_lines;
-    uint16_t* omask = (odd ? a.mask[0] : a.mask[1]) + tile_lines;
+    const char* in = reinterpret_cast<const char*>(odd ? a.slab[1] : a.slab[0]) + tile_lines * kLineBytes + lane * 32;
+    char* out = reinterpret_cast<char*>(odd ? a.slab[0] : a.slab[1]) + tile_lines * kLineBytes + lane * 32;
+    const uint32_t* imask = (odd ? a.mask[1] : a.mask[0]) + tile_lines;
+    uint32_t* omask = (odd ? a.mask[0] : a.mask[1]) + tile_lines;
     const unsigned zoff = (unsigned)(a.ld - 1) * kLineBytes;
     const int jw = j0 + warp;
     if (jw >= j1) return;
@@ -322,7 +341,7 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
     const int total = n_cols * nb;
     if (total == 0) {  // zero-width layer: every output is an empty chain
         for (int j = jw; j < j1; j += kWarps)
-            if (lane == 0) omask[j] = 0;
+            if (lane == 0) omask[j] = 0u;
         return;
     }
     auto slot_ptr = [&](int b) {
@@ -338,65 +357,90 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
         k1 = __ldg(L.idx + slot_ptr(1));
         w1 = __ldg(L.val + slot_ptr(1));
     }
-    unsigned m0 = k0 >= 0 ? (unsigned)imask[k0] : 0u;
+    unsigned m0 = k0 >= 0 ? imask[k0] : 0u;
     T acc[RPL];
-    uint32_t alive_acc[RPL];
+    unsigned alive_bits = 0u;
 #pragma unroll
-    for (int c = 0; c < RPL; ++c) {
-        acc[c] = T(0);
-        alive_acc[c] = 0u;
-    }
+    for (int c = 0; c < RPL; ++c) acc[c] = T(0);
     for (int b = 0; b < total; ++b) {
         // issue the next loads before working on batch b
         if (b + 2 < total) {
             k2 = __ldg(L.idx + slot_ptr(b + 2));
             w2 = __ldg(L.val + slot_ptr(b + 2));
         }
-        const unsigned m1 = (b + 1 < total && k1 >= 0) ? (unsigned)imask[k1] : 0u;
+        const unsigned m1 = (b + 1 < total && k1 >= 0) ? imask[k1] : 0u;
 
         const unsigned live = __ballot_sync(0xffffffffu, m0 != 0u);
-        if (m0) {
+        const int n = __popc(live);
+        // the list is padded up to a multiple of GB with entries that read
+        // the zero line with weight 0 (adds +0, never changes a chain), so
+        // the gather loops below carry no per-slot guards
+        const int npad = (n + GB - 1) / GB * GB;
+        {
             SlotEntry<T> e;
-            e.off = (unsigned)k0 * kLineBytes;
-            e.mask = m0;
-            e.w = w0;
-            wlist[__popc(live & ((1u << lane) - 1u))] = e;
+            int at;
+            if (m0) {
+                e.off = (unsigned)k0 * kLineBytes;
+                e.mask = m0;
+                e.w = w0;
+                at = __popc(live & (lbit - 1u));
+            } else {
+                e.off = zoff;
+                e.mask = 0xFFFFFFFFu;
+                e.w = T(0);
+                at = n + __popc(~live & (lbit - 1u));
+            }
+            if (at < npad) wlist[at] = e;
         }
         __syncwarp();
-        const int n = __popc(live);
-        for (int i0 = 0; i0 < n; i0 += GB) {
-            T y[GB][RPL];
+        auto issue = [&](T (&y)[GB][RPL], int i0) {
 #pragma unroll
             for (int u = 0; u < GB; ++u) {
-                if (i0 + u < n) {
-                    const unsigned off = (wlist[i0 + u].mask & sbit) ? wlist[i0 + u].off : zoff;
-                    ld16(y[u], in + off);
-                }
+                const SlotEntry<T> e = wlist[i0 + u];
+                ld32(y[u], in + ((e.mask & lbit) ? e.off : zoff));
             }
+        };
+        auto consume = [&](const T (&y)[GB][RPL], int i0) {
 #pragma unroll
             for (int u = 0; u < GB; ++u) {
-                if (i0 + u < n) {
-                    const T w = wlist[i0 + u].w;
+                const T w = wlist[i0 + u].w;
 #pragma unroll
-                    for (int c = 0; c < RPL; ++c) acc[c] = A::muladd(y[u][c], w, acc[c]);
-                }
+                for (int c = 0; c < RPL; ++c) acc[c] = A::muladd(y[u][c], w, acc[c]);
+            }
+        };
+        if (DBUF) {
+            // the next sub-batch's loads are in flight while this one is consumed
+            T ya[GB][RPL], yb[GB][RPL];
+            if (npad) issue(ya, 0);
+            for (int i0 = 0; i0 < npad; i0 += 2 * GB) {
+                if (i0 + GB < npad) issue(yb, i0 + GB);
+                consume(ya, i0);
+                if (i0 + GB >= npad) break;
+                if (i0 + 2 * GB < npad) issue(ya, i0 + 2 * GB);
+                consume(yb, i0 + GB);
+            }
+        } else {
+            for (int i0 = 0; i0 < npad; i0 += GB) {
+                T y[GB][RPL];
+                issue(y, i0);
+                consume(y, i0);
             }
         }
         __syncwarp();
         if (b % nb == nb - 1) {  // column complete: epilogue
             const int j = jw + (b / nb) * kWarps;
             T v[RPL];
-            bool any = false;
+            unsigned bits = 0u;
 #pragma unroll
             for (int c = 0; c < RPL; ++c) {
                 v[c] = a.epilogue ? bias_relu_clamp(acc[c], L.bias, a.ymax) : acc[c];
-                any |= v[c] != T(0);
-                alive_acc[c] |= __ballot_sync(0xffffffffu, v[c] != T(0));
+                bits |= (v[c] != T(0)) ? (1u << c) : 0u;
                 acc[c] = T(0);
             }
-            const unsigned om = sector_mask(__ballot_sync(0xffffffffu, any));
-            if (om & sbit) st16(out + (size_t)j * kLineBytes, v);
-            if (lane == 0) __stcs(reinterpret_cast<unsigned short*>(omask + j), (unsigned short)om);
+            const unsigned om = __ballot_sync(0xffffffffu, bits != 0u);
+            if (bits) st32(out + (size_t)j * kLineBytes, v);
+            if (lane == 0) __stcs(omask + j, om);
+            alive_bits |= bits;
         }
         k0 = k1;
         w0 = w1;
@@ -404,29 +448,21 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
         k1 = k2;
         w1 = w2;
     }
-    // live rows of this warp's columns -> the tile's alive words
-    bool any_alive = false;
-#pragma unroll
-    for (int c = 0; c < RPL; ++c) any_alive |= alive_acc[c] != 0u;
-    if (lane == 0 && any_alive) {
-        uint32_t* aw = a.alive + ((size_t)(l + 1) * a.n_tiles + t) * AW;
-#pragma unroll
-        for (int c = 0; c < RPL; ++c)
-            if (alive_acc[c]) atomicOr(&aw[c], alive_acc[c]);
-        if (atomicOr(&aw[RPL], 1u) == 0u) atomicAdd(&a.tile_count[l + 1], 1);
-    }
+    // live rows of this warp's columns -> the tile's row bitmap
+    if (__any_sync(0xffffffffu, alive_bits != 0u))
+        publish_alive<T>(a.alive + ((size_t)(l + 1) * a.n_tiles + t) * AW, alive_bits, &a.tile_count[l + 1]);
 }
 
-// GB = lines gathered per batch (loads in flight per warp); fewer CTAs per
-// SM for the deeper batch so its registers fit.
-template <typename T, int GB>
-__global__ void __launch_bounds__(kThreads, GB <= 8 ? 3 : 2) net_kernel(NetArgs<T> a) {
+// GB = lines gathered per sub-batch per warp.
+template <typename T, int GB, bool DBUF>
+__global__ void __launch_bounds__(kThreads, (DBUF ? 2 * GB : GB) * 8 <= 32 ? 3 : 2)  // y registers
+    net_kernel(NetArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem[];
     int32_t* tiles = reinterpret_cast<int32_t*>(smem);
     __shared__ SlotEntry<T> s_list[kWarps][32];
     __shared__ int s_count;
     __shared__ int s_scan[kWarps + 1];
-    constexpr int RPL = rows_per_lane<T>(), AW = alive_words<T>();
+    constexpr int AW = alive_words<T>();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned nb = gridDim.x;
     if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[0] = globaltimer();
@@ -442,7 +478,7 @@ __global__ void __launch_bounds__(kThreads, GB <= 8 ? 3 : 2) net_kernel(NetArgs<
         __syncthreads();
         for (int base = 0; base < a.n_tiles; base += kThreads) {
             const int t = base + tid;
-            const bool live = t < a.n_tiles && __ldcg(&alive_in[(size_t)t * AW + RPL]) != 0u;
+            const bool live = t < a.n_tiles && __ldcg(&alive_in[(size_t)t * AW + AW - 1]) != 0u;
             const unsigned b = __ballot_sync(0xffffffffu, live);
             if (lane == 0) s_scan[warp] = __popc(b);
             __syncthreads();
@@ -467,9 +503,9 @@ __global__ void __launch_bounds__(kThreads, GB <= 8 ? 3 : 2) net_kernel(NetArgs<
         const long long items = (long long)count * nblk;
         for (long long it = blockIdx.x; it < items; it += gridDim.x) {
             const int t = tiles[it / nblk];
-            const int b = (int)(it % nblk);
-            const int j0 = b * a.jb, j1 = min(a.n_out, j0 + a.jb);
-            layer_item<T, GB>(a, L, l, t, j0, j1, s_list[warp]);
+            const int bb = (int)(it % nblk);
+            const int j0 = bb * a.jb, j1 = min(a.n_out, j0 + a.jb);
+            layer_item<T, GB, DBUF>(a, L, l, t, j0, j1, s_list[warp]);
         }
         grid_barrier(a.bar, nb);
         if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[l + 1] = globaltimer();
@@ -480,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, GB <= 8 ? 3 : 2) net_kernel(NetArgs<
 // each lane its RPL rows: pass 1 (pos == null) counts entries, pass 2 writes
 // (column, value) in ascending column order at pos[tile * TR + row].
 template <typename T>
-__global__ void extract_kernel(const T* __restrict__ slab, const uint16_t* __restrict__ mask, int ld,
+__global__ void extract_kernel(const T* __restrict__ slab, const uint32_t* __restrict__ mask, int ld,
                                int n_cols, int n_tiles, const int64_t* __restrict__ pos,
                                int32_t* __restrict__ counts, int32_t* __restrict__ cols_out,
                                T* __restrict__ vals_out) {
@@ -488,10 +524,10 @@ __global__ void extract_kernel(const T* __restrict__ slab, const uint16_t* __res
     const int lane = threadIdx.x & 31;
     const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int n_warps = (gridDim.x * blockDim.x) >> 5;
-    const unsigned sbit = 1u << (lane >> 1);
+    const unsigned lbit = 1u << lane;
     for (int t = warp_global; t < n_tiles; t += n_warps) {
         const T* s = slab + (size_t)t * ld * TR + lane * RPL;
-        const uint16_t* m = mask + (size_t)t * ld;
+        const uint32_t* m = mask + (size_t)t * ld;
         int64_t at[RPL];
         int c[RPL];
 #pragma unroll
@@ -500,7 +536,7 @@ __global__ void extract_kernel(const T* __restrict__ slab, const uint16_t* __res
             c[q] = 0;
         }
         for (int k = 0; k < n_cols; ++k) {
-            if (!(m[k] & sbit)) continue;
+            if (!(m[k] & lbit)) continue;
 #pragma unroll
             for (int q = 0; q < RPL; ++q) {
                 const T v = s[(size_t)k * TR + q];
