@@ -428,6 +428,9 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     CK(cudaMemsetAsync(tile_count, 0, (nl + 1) * 4, net->stream));
     CK(cudaMemsetAsync(stamps, 0, (nl + 1) * 8, net->stream));
     CK(cudaMemsetAsync(net->bar, 0, 8, net->stream));
+    unsigned* work = nullptr;
+    CK(cudaMalloc(&work, std::max<int64_t>(nl, 1) * 4));
+    CK(cudaMemsetAsync(work, 0, std::max<int64_t>(nl, 1) * 4, net->stream));
 
     NetArgs<T> a{};
     a.n_in = (int)n_in;
@@ -445,9 +448,10 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     a.alive = net->alive;
     a.tile_count = tile_count;
     a.bar = net->bar;
+    a.work = work;
     a.stamps = net->layer_timing ? stamps : nullptr;
     a.jb = env_int("SDNN_JB", net->jb);
-    const int kc = env_int("SDNN_DENSIFY_KC", 48);  // input neurons per staging chunk
+    const int kc = env_int("SDNN_DENSIFY_KC", 96);  // input neurons per staging chunk
     const size_t dsmem = (size_t)kc * kLineBytes;
     const void* dfn = (const void*)densify_kernel<T>;
     CK(cudaFuncSetAttribute(dfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
@@ -510,6 +514,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     cudaFree(tile_count);
     cudaFree(live);
     cudaFree(stamps);
+    cudaFree(work);
     cudaFree(net->rowid);
     net->rowid = nullptr;
     return SDNN_OK;

@@ -146,6 +146,7 @@ struct NetArgs {
     uint32_t* alive;      // [L + 1][n_tiles][alive_words] live-row bitmap + flag
     int32_t* tile_count;  // [L + 1] tiles with any live row
     unsigned* bar;        // grid barrier {count, generation}
+    unsigned* work;       // [L] per-layer work-item counters (zeroed)
     unsigned long long* stamps;  // [L + 1] globaltimer after each layer, or null
     int jb;               // outputs per work item
 };
@@ -462,6 +463,7 @@ __global__ void __launch_bounds__(kThreads, (DBUF ? 2 * GB : GB) * 8 <= 32 ? 3 :
     __shared__ SlotEntry<T> s_list[kWarps][32];
     __shared__ int s_count;
     __shared__ int s_scan[kWarps + 1];
+    __shared__ long long s_item;
     constexpr int AW = alive_words<T>();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned nb = gridDim.x;
@@ -501,7 +503,15 @@ __global__ void __launch_bounds__(kThreads, (DBUF ? 2 * GB : GB) * 8 <= 32 ? 3 :
         const LayerDesc<T> L = a.layers[l];
         const int nblk = (a.n_out + a.jb - 1) / a.jb;
         const long long items = (long long)count * nblk;
-        for (long long it = blockIdx.x; it < items; it += gridDim.x) {
+        // items are handed out in order from a counter, so all CTAs work on
+        // a narrow window of tiles and the tiles' input lines stay in L2
+        // across the 32 columns that gather each of them
+        for (;;) {
+            if (tid == 0) s_item = (long long)atomicAdd(&a.work[l], 1u);
+            __syncthreads();
+            const long long it = s_item;
+            __syncthreads();
+            if (it >= items) break;
             const int t = tiles[it / nblk];
             const int bb = (int)(it % nblk);
             const int j0 = bb * a.jb, j1 = min(a.n_out, j0 + a.jb);
