@@ -108,7 +108,8 @@ struct sdnn_net {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // run scratch, grown on demand
     void* slab[2] = {nullptr, nullptr};
-    uint32_t* mask[2] = {nullptr, nullptr};
+    uint2* meta[2] = {nullptr, nullptr};
+    void* zero = nullptr;  // one all-zero 32-byte sector
     int64_t tcap = 0;  // tiles per buffer
     int64_t tcap_lines = 0;
     int32_t* rowid = nullptr;
@@ -226,14 +227,14 @@ int ensure_tiles(sdnn_net* net, int64_t tiles, int64_t ld) {
     if (tiles > net->tcap || !net->slab[0] || ld * std::max<int64_t>(tiles, 1) > net->tcap_lines) {
         for (int b = 0; b < 2; ++b) {
             if (net->slab[b]) CK(cudaFree(net->slab[b]));
-            if (net->mask[b]) CK(cudaFree(net->mask[b]));
+            if (net->meta[b]) CK(cudaFree(net->meta[b]));
             net->slab[b] = nullptr;
-            net->mask[b] = nullptr;
+            net->meta[b] = nullptr;
         }
         const int64_t lines = std::max<int64_t>(tiles, 1) * ld;
         for (int b = 0; b < 2; ++b) {
             CK(cudaMalloc(&net->slab[b], lines * kLineBytes));
-            CK(cudaMalloc(&net->mask[b], lines * sizeof(uint32_t)));
+            CK(cudaMalloc(&net->meta[b], lines * sizeof(uint2)));
         }
         net->tcap = tiles;
         net->tcap_lines = lines;
@@ -247,8 +248,8 @@ int64_t wave_rows(sdnn_net* net, int64_t n_rows, int64_t ld, int tr) {
     if (forced > 0) return std::min(forced, std::max<int64_t>(n_rows, 1));
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
-    const int64_t per_tile = 2 * ld * (kLineBytes + 4);
-    int64_t held = net->tcap_lines * (kLineBytes + 4) * 2;
+    const int64_t per_tile = 2 * ld * (kLineBytes + 8);
+    int64_t held = net->tcap_lines * (kLineBytes + 8) * 2;
     int64_t avail = (int64_t)free_b + held - (int64_t)(2ull << 30);
     int64_t w = std::max<int64_t>(1, avail / per_tile) * tr;
     return std::min(w, std::max<int64_t>(n_rows, 1));
@@ -303,7 +304,7 @@ void assemble(sdnn_result* res, std::vector<Piece>& pieces) {
 
 // Final Y of the tiles that are still live -> host CSR pieces.
 template <typename T>
-int extract(sdnn_net* net, const T* slab, const uint32_t* mask, int ld, int n_cols, int64_t n_tiles,
+int extract(sdnn_net* net, const T* slab, const uint2* meta, int ld, int n_cols, int64_t n_tiles,
             const std::vector<uint32_t>& alive, const std::vector<int32_t>& rowid, Piece& p) {
     constexpr int TR = tile_rows<T>(), AW = alive_words<T>(), RPL = rows_per_lane<T>();
     p.rows.assign(rowid.begin(), rowid.end());
@@ -316,7 +317,7 @@ int extract(sdnn_net* net, const T* slab, const uint32_t* mask, int ld, int n_co
     const int64_t lanes = n_tiles * TR;
     CK(cudaMalloc(&counts, lanes * 4));
     const int grid = (int)std::min<int64_t>((n_tiles + 7) / 8, (int64_t)net->sm_count * 16);
-    extract_kernel<T><<<grid, 256, 0, net->stream>>>(slab, mask, ld, n_cols, (int)n_tiles, nullptr, counts,
+    extract_kernel<T><<<grid, 256, 0, net->stream>>>(slab, meta, ld, n_cols, (int)n_tiles, nullptr, counts,
                                                      nullptr, nullptr);
     CK(cudaGetLastError());
     std::vector<int32_t> cnt(lanes);
@@ -347,7 +348,7 @@ int extract(sdnn_net* net, const T* slab, const uint32_t* mask, int ld, int n_co
         while (j + 1 < live_ids.size() && live_ids[j + 1] == live_ids[j] + 1) ++j;
         const int64_t t0 = live_ids[i], nt = live_ids[j] - t0 + 1;
         const int g = (int)std::min<int64_t>((nt + 7) / 8, (int64_t)net->sm_count * 16);
-        extract_kernel<T><<<g, 256, 0, net->stream>>>(slab + (size_t)t0 * ld * TR, mask + (size_t)t0 * ld, ld, n_cols,
+        extract_kernel<T><<<g, 256, 0, net->stream>>>(slab + (size_t)t0 * ld * TR, meta + (size_t)t0 * ld, ld, n_cols,
                                                       (int)nt, pos + t0 * TR, nullptr, cols, vals);
         CK(cudaGetLastError());
         i = j + 1;
@@ -392,7 +393,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
              int64_t r0, int64_t r1, int64_t n_in, int64_t n_out, int want_y, sdnn_result* res,
              std::vector<int32_t>& final_rows, std::vector<Piece>& pieces, float& dev_ms) {
     constexpr int TR = tile_rows<T>(), RPL = rows_per_lane<T>(), AW = alive_words<T>();
-    const int64_t ld = std::max(n_in, n_out) + 1;  // + the zero line
+    const int64_t ld = std::max(n_in, n_out);
     const int64_t rows = r1 - r0;
     // ascending list of the wave's rows that hold an entry
     if (int rc = grow(net->rowlist, net->rcap, std::max<int64_t>(rows, TR), 4)) return rc;
@@ -428,6 +429,13 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     CK(cudaMemsetAsync(tile_count, 0, (nl + 1) * 4, net->stream));
     CK(cudaMemsetAsync(stamps, 0, (nl + 1) * 8, net->stream));
     CK(cudaMemsetAsync(net->bar, 0, 8, net->stream));
+    if (!net->zero) {
+        CK(cudaMalloc(&net->zero, 64));
+        CK(cudaMemset(net->zero, 0, 64));
+    }
+    uint32_t* heap = nullptr;
+    CK(cudaMalloc(&heap, (nl + 1) * tiles1 * 4));
+    CK(cudaMemsetAsync(heap, 0, (nl + 1) * tiles1 * 4, net->stream));
     unsigned* work = nullptr;
     CK(cudaMalloc(&work, std::max<int64_t>(nl, 1) * 4));
     CK(cudaMemsetAsync(work, 0, std::max<int64_t>(nl, 1) * 4, net->stream));
@@ -443,8 +451,10 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     a.n_tiles = (int)n_tiles;
     for (int b = 0; b < 2; ++b) {
         a.slab[b] = reinterpret_cast<T*>(net->slab[b]);
-        a.mask[b] = net->mask[b];
+        a.meta[b] = net->meta[b];
     }
+    a.heap = heap;
+    a.zero = reinterpret_cast<const T*>(net->zero);
     a.alive = net->alive;
     a.tile_count = tile_count;
     a.bar = net->bar;
@@ -474,7 +484,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
         const int dgrid = (int)std::min<int64_t>(n_tiles, (int64_t)net->sm_count * 4);
         densify_kernel<T><<<dgrid, kDensifyThreads, dsmem, net->stream>>>(
             batch->off, batch->cols, reinterpret_cast<const T*>(batch->vals), net->rowid, (int)n_in, (int)ld,
-            (int)n_tiles, kc, a.slab[0], a.slab[1], a.mask[0], net->alive, tile_count);
+            (int)n_tiles, kc, a.slab[0], a.meta[0], heap, net->alive, tile_count);
         CK(cudaGetLastError());
         res->launches += 1;
     }
@@ -506,7 +516,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     if (want_y) {
         Piece p;
         const int last = (int)(nl & 1);  // layer nl-1 wrote buffer nl & 1
-        if (int rc = extract<T>(net, reinterpret_cast<const T*>(net->slab[last]), net->mask[last], (int)ld,
+        if (int rc = extract<T>(net, reinterpret_cast<const T*>(net->slab[last]), net->meta[last], (int)ld,
                                 (int)n_out, n_tiles, alive_last, rowid, p))
             return rc;
         pieces.push_back(std::move(p));
@@ -515,6 +525,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     cudaFree(live);
     cudaFree(stamps);
     cudaFree(work);
+    cudaFree(heap);
     cudaFree(net->rowid);
     net->rowid = nullptr;
     return SDNN_OK;
@@ -524,7 +535,7 @@ template <typename T>
 int run_impl(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first, int64_t nl, int want_y,
              int epilogue, int64_t n_in, int64_t n_out, sdnn_result* res) {
     const int64_t B = batch->n_rows;
-    const int64_t ld = std::max(n_in, n_out) + 1;
+    const int64_t ld = std::max(n_in, n_out);
     if (int rc = sync_descs<T>(net)) return rc;
     const int64_t wave = wave_rows(net, B, ld, tile_rows<T>());
     res->n_rows = B;
@@ -690,8 +701,9 @@ void sdnn_net_destroy(sdnn_net* net) {
     cudaFree(net->descs);
     for (int b = 0; b < 2; ++b) {
         cudaFree(net->slab[b]);
-        cudaFree(net->mask[b]);
+        cudaFree(net->meta[b]);
     }
+    cudaFree(net->zero);
     cudaFree(net->rowid);
     cudaFree(net->rowlist);
     cudaFree(net->alive);

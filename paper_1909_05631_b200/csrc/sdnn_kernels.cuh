@@ -21,16 +21,17 @@
 // changing a bit.
 //
 // Activations: "tiles" of TR live rows (256 in float32, 128 in float64)
-// stored neuron-major: one 1 KB line per (tile, neuron),
-//     slab[(tile * ld + k) * TR + r],
-// lane l of a warp owns rows l*RPL .. l*RPL+RPL-1 (RPL = 32 B / sizeof(T)),
-// i.e. exactly one 32-byte sector, read with one 256-bit load.  A warp
-// computes one output column of a tile: per weight slot it gathers one whole
-// line, so one weight slot serves TR rows.  A 32-bit mask per (tile, neuron)
-// flags which lanes' sectors hold a nonzero; zero sectors are not stored,
-// and their gathers read the tile's dedicated zero line (line ld-1) instead;
-// slots whose whole line is zero are dropped from the warp's slot list
-// before any gather.
+// stored neuron-major.  The line of one (tile, neuron) holds TR values, 32
+// lanes x one 32-byte sector: lane l owns rows l*RPL .. l*RPL+RPL-1
+// (RPL = 32 B / sizeof(T)), read with one 256-bit load.  Lines are stored
+// sector-compressed: only sectors holding a nonzero are kept, packed in lane
+// order, in the tile's sector heap; meta[(tile, neuron)] = {lane mask of the
+// kept sectors, heap index of the first}.  A warp computes one output column
+// of a tile: per weight slot it gathers one line (each live lane its sector,
+// dead lanes read a shared zero sector), so one weight slot serves TR rows.
+// Slots whose whole line is zero are dropped from the warp's slot list
+// before any gather.  Packing keeps a tile's L2 footprint at its live data,
+// which is what lets the 32 columns that read each line hit in L2.
 //
 // A cooperative persistent kernel walks all layers with one grid barrier per
 // live layer and a per-layer live-tile count, so layers after the last live
@@ -119,8 +120,8 @@ __device__ __forceinline__ void st32_bits(char* p, const uint4& a, const uint4& 
 // One live slot of a warp's compacted slot list (16 bytes).
 template <typename T>
 struct __align__(16) SlotEntry {
-    unsigned off;   // line byte offset k * 1024
-    unsigned mask;  // lanes whose sector of that line holds a nonzero
+    unsigned base;  // heap index of the line's first kept sector
+    unsigned mask;  // lanes whose sector of that line is kept (nonzero)
     T w;            // weight
 };
 
@@ -135,14 +136,16 @@ struct LayerDesc {
 template <typename T>
 struct NetArgs {
     int n_in, n_out;      // input lines per tile, outputs per layer
-    int ld;               // lines per tile (>= n_in, n_out, plus the zero line)
+    int ld;               // lines per tile (>= n_in, n_out); heap = ld * 32 sectors
     int L;
     const LayerDesc<T>* layers;
     T ymax;
     int epilogue;         // 1: bias/ReLU/clamp; 0: raw Z (engine.spmm)
     int n_tiles;
-    T* slab[2];           // [n_tiles][ld][TR]
-    uint32_t* mask[2];    // [n_tiles][ld] lanes whose sector is nonzero
+    T* slab[2];           // [n_tiles][ld * 32 sectors of 32 B] sector heaps
+    uint2* meta[2];       // [n_tiles][ld] {kept-sector lane mask, heap index}
+    uint32_t* heap;       // [L + 1][n_tiles] sectors used in each layer's heap
+    const T* zero;        // one all-zero 32-byte sector
     uint32_t* alive;      // [L + 1][n_tiles][alive_words] live-row bitmap + flag
     int32_t* tile_count;  // [L + 1] tiles with any live row
     unsigned* bar;        // grid barrier {count, generation}
@@ -214,8 +217,8 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_kernel(const int64_t*
                                                                   const int32_t* __restrict__ csr_cols,
                                                                   const T* __restrict__ csr_vals,
                                                                   const int32_t* __restrict__ rowid, int n_in,
-                                                                  int ld, int n_tiles, int kc, T* slab0, T* slab1,
-                                                                  uint32_t* mask0, uint32_t* alive0,
+                                                                  int ld, int n_tiles, int kc, T* slab0,
+                                                                  uint2* meta0, uint32_t* heap0, uint32_t* alive0,
                                                                   int32_t* tile_count0) {
     extern __shared__ __align__(16) unsigned char dsm[];
     constexpr int TR = tile_rows<T>(), AW = alive_words<T>();
@@ -223,6 +226,7 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_kernel(const int64_t*
     T* stage = reinterpret_cast<T*>(dsm);                  // [kc][TR]
     __shared__ int64_t s_pos[TR], s_end[TR];               // window base, row end
     __shared__ uint32_t s_alive[AW];
+    __shared__ unsigned s_heap;                            // sectors used so far
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
     {
@@ -231,6 +235,7 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_kernel(const int64_t*
     }
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         if (tid < AW) s_alive[tid] = 0u;
+        if (tid == 0) s_heap = 0u;
         __syncthreads();
         for (int r = tid; r < TR; r += blockDim.x) {
             const int row = rowid[(size_t)t * TR + r];
@@ -253,19 +258,14 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_kernel(const int64_t*
             vb[i] = q < s_end[r] ? csr_vals[q] : T(0);
         }
         char* s0 = reinterpret_cast<char*>(slab0 + (size_t)t * ld * TR);
-        char* s1 = reinterpret_cast<char*>(slab1 + (size_t)t * ld * TR);
-        if (warp == 0) {
-            st32_bits(s0 + (size_t)(ld - 1) * kLineBytes + lane * 32, z4, z4);
-            st32_bits(s1 + (size_t)(ld - 1) * kLineBytes + lane * 32, z4, z4);
-        }
-        uint32_t* gm = mask0 + (size_t)t * ld;
+        uint2* gm = meta0 + (size_t)t * ld;
         for (int k0 = 0; k0 < n_in; k0 += kc) {
             const int kn = min(kc, n_in - k0);
             bool mine = false;
 #pragma unroll
             for (int i = 0; i < RW; ++i) mine |= cb[i] < k0 + kn;
             if (!__syncthreads_or(mine)) {  // the whole chunk is zero for every row
-                for (int k = tid; k < kn; k += blockDim.x) gm[k0 + k] = 0u;
+                for (int k = tid; k < kn; k += blockDim.x) gm[k0 + k] = make_uint2(0u, 0u);
                 continue;
             }
 #pragma unroll
@@ -297,15 +297,21 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_kernel(const int64_t*
 #pragma unroll
                 for (int c = 0; c < rows_per_lane<T>(); ++c) any |= sv[c] != T(0);
                 const unsigned m = __ballot_sync(0xffffffffu, any);
-                if (any) st32_bits(s0 + (size_t)(k0 + k) * kLineBytes + lane * 32, a, b);
-                if (lane == 0) gm[k0 + k] = m;
+                unsigned base = 0u;
+                if (lane == 0 && m) base = atomicAdd(&s_heap, (unsigned)__popc(m));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (any) st32_bits(s0 + (size_t)(base + __popc(m & ((1u << lane) - 1u))) * 32, a, b);
+                if (lane == 0) gm[k0 + k] = make_uint2(m, base);
                 src[0] = z4;  // re-zero for the next chunk
                 src[1] = z4;
             }
         }
         __syncthreads();
         if (tid < AW) alive0[(size_t)t * AW + tid] = s_alive[tid];
-        if (tid == 0 && s_alive[AW - 1]) atomicAdd(tile_count0, 1);
+        if (tid == 0) {
+            heap0[t] = s_heap;
+            if (s_alive[AW - 1]) atomicAdd(tile_count0, 1);
+        }
     }
 }
 
@@ -330,11 +336,13 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
     // select, not index: a runtime index into the parameter struct would
     // force a local-memory copy of it
     const bool odd = l & 1;
-    const char* in = reinterpret_cast<const char*>(odd ? a.slab[1] : a.slab[0]) + tile_lines * kLineBytes + lane * 32;
-    char* out = reinterpret_cast<char*>(odd ? a.slab[0] : a.slab[1]) + tile_lines * kLineBytes + lane * 32;
-    const uint32_t* imask = (odd ? a.mask[1] : a.mask[0]) + tile_lines;
-    uint32_t* omask = (odd ? a.mask[0] : a.mask[1]) + tile_lines;
-    const unsigned zoff = (unsigned)(a.ld - 1) * kLineBytes;
+    const char* in = reinterpret_cast<const char*>(odd ? a.slab[1] : a.slab[0]) + tile_lines * kLineBytes;
+    char* out = reinterpret_cast<char*>(odd ? a.slab[0] : a.slab[1]) + tile_lines * kLineBytes;
+    const uint2* imeta = (odd ? a.meta[1] : a.meta[0]) + tile_lines;
+    uint2* ometa = (odd ? a.meta[0] : a.meta[1]) + tile_lines;
+    uint32_t* heap_out = a.heap + (size_t)(l + 1) * a.n_tiles + t;
+    const char* zsec = reinterpret_cast<const char*>(a.zero);
+    const unsigned below = lbit - 1u;
     const int jw = j0 + warp;
     if (jw >= j1) return;
     const int nb = L.wp / 32;  // batches per column
@@ -342,7 +350,7 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
     const int total = n_cols * nb;
     if (total == 0) {  // zero-width layer: every output is an empty chain
         for (int j = jw; j < j1; j += kWarps)
-            if (lane == 0) omask[j] = 0u;
+            if (lane == 0) ometa[j] = make_uint2(0u, 0u);
         return;
     }
     auto slot_ptr = [&](int b) {
@@ -358,7 +366,7 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
         k1 = __ldg(L.idx + slot_ptr(1));
         w1 = __ldg(L.val + slot_ptr(1));
     }
-    unsigned m0 = k0 >= 0 ? imask[k0] : 0u;
+    uint2 m0 = k0 >= 0 ? imeta[k0] : make_uint2(0u, 0u);
     T acc[RPL];
     unsigned alive_bits = 0u;
 #pragma unroll
@@ -369,9 +377,9 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
             k2 = __ldg(L.idx + slot_ptr(b + 2));
             w2 = __ldg(L.val + slot_ptr(b + 2));
         }
-        const unsigned m1 = (b + 1 < total && k1 >= 0) ? imask[k1] : 0u;
+        const uint2 m1 = (b + 1 < total && k1 >= 0) ? imeta[k1] : make_uint2(0u, 0u);
 
-        const unsigned live = __ballot_sync(0xffffffffu, m0 != 0u);
+        const unsigned live = __ballot_sync(0xffffffffu, m0.x != 0u);
         const int n = __popc(live);
         // the list is padded up to a multiple of GB with entries that read
         // the zero line with weight 0 (adds +0, never changes a chain), so
@@ -380,16 +388,16 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
         {
             SlotEntry<T> e;
             int at;
-            if (m0) {
-                e.off = (unsigned)k0 * kLineBytes;
-                e.mask = m0;
+            if (m0.x) {
+                e.base = m0.y;
+                e.mask = m0.x;
                 e.w = w0;
-                at = __popc(live & (lbit - 1u));
-            } else {
-                e.off = zoff;
-                e.mask = 0xFFFFFFFFu;
+                at = __popc(live & below);
+            } else {  // padding: no lane live -> every lane reads the zero sector
+                e.base = 0u;
+                e.mask = 0u;
                 e.w = T(0);
-                at = n + __popc(~live & (lbit - 1u));
+                at = n + __popc(~live & below);
             }
             if (at < npad) wlist[at] = e;
         }
@@ -398,7 +406,7 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
 #pragma unroll
             for (int u = 0; u < GB; ++u) {
                 const SlotEntry<T> e = wlist[i0 + u];
-                ld32(y[u], in + ((e.mask & lbit) ? e.off : zoff));
+                ld32(y[u], (e.mask & lbit) ? in + (size_t)(e.base + __popc(e.mask & below)) * 32 : zsec);
             }
         };
         auto consume = [&](const T (&y)[GB][RPL], int i0) {
@@ -439,8 +447,11 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
                 acc[c] = T(0);
             }
             const unsigned om = __ballot_sync(0xffffffffu, bits != 0u);
-            if (bits) st32(out + (size_t)j * kLineBytes, v);
-            if (lane == 0) __stcs(omask + j, om);
+            unsigned hb = 0u;
+            if (lane == 0 && om) hb = atomicAdd(heap_out, (unsigned)__popc(om));
+            hb = __shfl_sync(0xffffffffu, hb, 0);
+            if (bits) st32(out + (size_t)(hb + __popc(om & below)) * 32, v);
+            if (lane == 0) ometa[j] = make_uint2(om, hb);
             alive_bits |= bits;
         }
         k0 = k1;
@@ -526,7 +537,7 @@ __global__ void __launch_bounds__(kThreads, (DBUF ? 2 * GB : GB) * 8 <= 32 ? 3 :
 // each lane its RPL rows: pass 1 (pos == null) counts entries, pass 2 writes
 // (column, value) in ascending column order at pos[tile * TR + row].
 template <typename T>
-__global__ void extract_kernel(const T* __restrict__ slab, const uint32_t* __restrict__ mask, int ld,
+__global__ void extract_kernel(const T* __restrict__ slab, const uint2* __restrict__ meta, int ld,
                                int n_cols, int n_tiles, const int64_t* __restrict__ pos,
                                int32_t* __restrict__ counts, int32_t* __restrict__ cols_out,
                                T* __restrict__ vals_out) {
@@ -536,8 +547,8 @@ __global__ void extract_kernel(const T* __restrict__ slab, const uint32_t* __res
     const int n_warps = (gridDim.x * blockDim.x) >> 5;
     const unsigned lbit = 1u << lane;
     for (int t = warp_global; t < n_tiles; t += n_warps) {
-        const T* s = slab + (size_t)t * ld * TR + lane * RPL;
-        const uint32_t* m = mask + (size_t)t * ld;
+        const T* s = slab + (size_t)t * ld * TR;
+        const uint2* m = meta + (size_t)t * ld;
         int64_t at[RPL];
         int c[RPL];
 #pragma unroll
@@ -546,10 +557,12 @@ __global__ void extract_kernel(const T* __restrict__ slab, const uint32_t* __res
             c[q] = 0;
         }
         for (int k = 0; k < n_cols; ++k) {
-            if (!(m[k] & lbit)) continue;
+            const uint2 mk = m[k];
+            if (!(mk.x & lbit)) continue;
+            const T* sec = s + (size_t)(mk.y + __popc(mk.x & (lbit - 1u))) * RPL;
 #pragma unroll
             for (int q = 0; q < RPL; ++q) {
-                const T v = s[(size_t)k * TR + q];
+                const T v = sec[q];
                 if (v != T(0)) {
                     if (pos) {
                         cols_out[at[q]] = k;
