@@ -87,6 +87,9 @@ int sdnn_net_weight_bytes(const sdnn_net *net, int64_t *bytes);
 int sdnn_batch_upload(sdnn_net *net, int64_t n_rows, const int64_t *y_off,
                       const int64_t *y_cols, const double *y_vals, sdnn_batch **out);
 void sdnn_batch_free(sdnn_batch *batch);
+/* Bytes the upload copied host -> device (offsets, columns as uint16 when
+ * the row length is <= 65536 else int32, values unless all are 1.0). */
+int sdnn_batch_h2d_bytes(const sdnn_batch *batch, int64_t *bytes);
 
 /* Run layers [first_layer, first_layer + n_layers) over a staged batch and
  * build the category list (the reference's timed region,

@@ -33,6 +33,7 @@ SIGNATURES = [
     ("sdnn_net_weight_bytes", cint, [vp, P(i64)]),
     ("sdnn_batch_upload", cint, [vp, i64, vp, vp, vp, P(vp)]),
     ("sdnn_batch_free", None, [vp]),
+    ("sdnn_batch_h2d_bytes", cint, [vp, P(i64)]),
     ("sdnn_run", cint, [vp, vp, dbl, i64, i64, P(vp)]),
     ("sdnn_run_y", cint, [vp, vp, dbl, i64, i64, P(vp)]),
     ("sdnn_infer", cint, [vp, i64, vp, vp, vp, dbl, P(vp)]),

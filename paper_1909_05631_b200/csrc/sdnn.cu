@@ -125,17 +125,20 @@ struct sdnn_net {
     int64_t ccap = 0;
     void* cub_tmp = nullptr;
     size_t cub_cap = 0;
-    void* pinned = nullptr;
+    void* pinned = nullptr;  // two staging buffers of pinned_cap bytes
     size_t pinned_cap = 0;
+    cudaEvent_t stage_ev[2] = {nullptr, nullptr};
     int layer_timing = 0;
 };
 
 struct sdnn_batch {
     sdnn_net* net = nullptr;
     int64_t n_rows = 0, nnz = 0, n_cols = 0;
+    int col_bytes = 4;        // 2: uint16 columns, 4: int32 columns
+    int64_t h2d_bytes = 0;    // bytes copied host -> device by the upload
     int64_t* off = nullptr;
-    int32_t* cols = nullptr;
-    void* vals = nullptr;
+    void* cols = nullptr;
+    void* vals = nullptr;     // null: every stored value is 1.0
 };
 
 struct sdnn_result {
@@ -483,8 +486,8 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     if (n_tiles) {
         const int dgrid = (int)std::min<int64_t>(n_tiles, (int64_t)net->sm_count * 4);
         densify_kernel<T><<<dgrid, kDensifyThreads, dsmem, net->stream>>>(
-            batch->off, batch->cols, reinterpret_cast<const T*>(batch->vals), net->rowid, (int)n_in, (int)ld,
-            (int)n_tiles, kc, a.slab[0], a.meta[0], heap, net->alive, tile_count);
+            batch->off, batch->cols, batch->col_bytes, reinterpret_cast<const T*>(batch->vals), net->rowid,
+            (int)n_in, (int)ld, (int)n_tiles, kc, a.slab[0], a.meta[0], heap, net->alive, tile_count);
         CK(cudaGetLastError());
         res->launches += 1;
     }
@@ -562,9 +565,15 @@ int run_impl(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
 }
 
 // Host CSR (int64/float64) -> device CSR (int64 offsets, int32 cols, T vals).
+// Host CSR (int64 columns, float64 values: the reference's FeatureBatch) ->
+// device CSR (int64 offsets, uint16 columns when n_cols <= 65536 else
+// int32, T values -- or no values at all when every value is 1.0, the
+// binary images of the challenge).  Converted by OpenMP threads chunk by
+// chunk into two pinned staging buffers while the previous chunk's copy is
+// in flight; device buffers come from the stream-ordered pool.
 template <typename T>
 int upload_csr(sdnn_net* net, int64_t n_rows, const int64_t* off, const int64_t* cols,
-               const double* vals, int64_t n_cols, sdnn_batch* b) {
+               const double* vals, int64_t n_cols, sdnn_batch* b, bool raw = false) {
     const int64_t nnz = n_rows > 0 ? off[n_rows] : 0;
     if (n_rows > 0 && off[0] != 0) return fail(SDNN_ERR_PARAMETER, "row_offsets[0] must be 0");
     for (int64_t i = 0; i < n_rows; ++i)
@@ -572,40 +581,79 @@ int upload_csr(sdnn_net* net, int64_t n_rows, const int64_t* off, const int64_t*
     b->n_rows = n_rows;
     b->nnz = nnz;
     b->n_cols = n_cols;
-    const size_t bytes = (size_t)nnz * (4 + sizeof(T));
-    if (bytes > net->pinned_cap) {
+    b->col_bytes = (n_cols <= 65536 && !raw) ? 2 : 4;
+    b->h2d_bytes = (n_rows + 1) * 8;
+    const int64_t chunk = std::max<int64_t>(1, env_int("SDNN_UPLOAD_CHUNK", 16 << 20));  // entries
+    const size_t stage_bytes = (size_t)std::min<int64_t>(chunk, std::max<int64_t>(nnz, 1)) * sizeof(T);
+    if (stage_bytes > net->pinned_cap) {
         if (net->pinned) CK(cudaFreeHost(net->pinned));
         net->pinned = nullptr;
-        CK(cudaMallocHost(&net->pinned, std::max<size_t>(bytes, 64)));
-        net->pinned_cap = std::max<size_t>(bytes, 64);
+        CK(cudaMallocHost(&net->pinned, 2 * stage_bytes));
+        net->pinned_cap = stage_bytes;
+        for (auto& e : net->stage_ev)
+            if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
-    int32_t* pc = reinterpret_cast<int32_t*>(net->pinned);
-    T* pv = reinterpret_cast<T*>(reinterpret_cast<char*>(net->pinned) + (size_t)nnz * 4);
-    std::vector<int> bad(1, 0);
-    parallel_for(nnz, [&](int64_t a, int64_t e) {
-        for (int64_t p = a; p < e; ++p) {
-            const int64_t c = cols[p];
-            if (c < 0 || c >= n_cols) bad[0] = 1;
-            pc[p] = (int32_t)c;
-            pv[p] = (T)vals[p];
-        }
-    });
-    if (bad[0]) return fail(SDNN_ERR_PARAMETER, "column index outside [0, %lld)", (long long)n_cols);
-    CK(cudaMalloc(&b->off, (n_rows + 1) * sizeof(int64_t)));
-    CK(cudaMalloc(&b->cols, std::max<int64_t>(nnz, 1) * 4));
-    CK(cudaMalloc(&b->vals, std::max<int64_t>(nnz, 1) * sizeof(T)));
+    char* stage[2] = {reinterpret_cast<char*>(net->pinned), reinterpret_cast<char*>(net->pinned) + net->pinned_cap};
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&b->off), (n_rows + 1) * sizeof(int64_t), net->stream));
+    CK(cudaMallocAsync(&b->cols, std::max<int64_t>(nnz, 1) * b->col_bytes, net->stream));
     CK(cudaMemcpyAsync(b->off, off, (n_rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, net->stream));
-    CK(cudaMemcpyAsync(b->cols, pc, nnz * 4, cudaMemcpyHostToDevice, net->stream));
-    CK(cudaMemcpyAsync(b->vals, pv, nnz * sizeof(T), cudaMemcpyHostToDevice, net->stream));
+    int bad = 0, binary = 1;
+    // pass 1: columns (and the binary check on values)
+    int buf = 0;
+    for (int64_t c0 = 0; c0 < nnz; c0 += chunk, buf ^= 1) {
+        const int64_t c1 = std::min(nnz, c0 + chunk);
+        CK(cudaEventSynchronize(net->stage_ev[buf]));  // the copy that last used this buffer
+        char* dst = stage[buf];
+        const int cb = b->col_bytes;
+        int chunk_bad = 0, chunk_bin = 1;
+#pragma omp parallel for reduction(| : chunk_bad) reduction(& : chunk_bin) schedule(static)
+        for (int64_t p = c0; p < c1; ++p) {
+            const int64_t c = cols[p];
+            chunk_bad |= (c < 0 || c >= n_cols);
+            chunk_bin &= (vals[p] == 1.0);
+            if (cb == 2)
+                reinterpret_cast<uint16_t*>(dst)[p - c0] = (uint16_t)c;
+            else
+                reinterpret_cast<int32_t*>(dst)[p - c0] = (int32_t)c;
+        }
+        bad |= chunk_bad;
+        binary &= chunk_bin;
+        CK(cudaMemcpyAsync(reinterpret_cast<char*>(b->cols) + c0 * cb, dst, (c1 - c0) * cb, cudaMemcpyHostToDevice,
+                           net->stream));
+        CK(cudaEventRecord(net->stage_ev[buf], net->stream));
+    }
+    if (bad) {
+        CK(cudaStreamSynchronize(net->stream));
+        return fail(SDNN_ERR_PARAMETER, "column index outside [0, %lld)", (long long)n_cols);
+    }
+    b->h2d_bytes += nnz * b->col_bytes;
+    b->vals = nullptr;
+    if (raw || env_int("SDNN_FORCE_VALUES", 0)) binary = 0;
+    if (!binary) {  // pass 2: values
+        CK(cudaMallocAsync(&b->vals, std::max<int64_t>(nnz, 1) * sizeof(T), net->stream));
+        for (int64_t c0 = 0; c0 < nnz; c0 += chunk, buf ^= 1) {
+            const int64_t c1 = std::min(nnz, c0 + chunk);
+            CK(cudaEventSynchronize(net->stage_ev[buf]));
+            T* dst = reinterpret_cast<T*>(stage[buf]);
+#pragma omp parallel for schedule(static)
+            for (int64_t p = c0; p < c1; ++p) dst[p - c0] = (T)vals[p];
+            CK(cudaMemcpyAsync(reinterpret_cast<T*>(b->vals) + c0, dst, (c1 - c0) * sizeof(T), cudaMemcpyHostToDevice,
+                               net->stream));
+            CK(cudaEventRecord(net->stage_ev[buf], net->stream));
+        }
+        b->h2d_bytes += nnz * (int64_t)sizeof(T);
+    }
     CK(cudaStreamSynchronize(net->stream));
     return SDNN_OK;
 }
 
 void free_batch(sdnn_batch* b) {
     if (!b) return;
-    cudaFree(b->off);
-    cudaFree(b->cols);
-    cudaFree(b->vals);
+    cudaStream_t st = b->net ? b->net->stream : nullptr;
+    if (b->off) cudaFreeAsync(b->off, st);
+    if (b->cols) cudaFreeAsync(b->cols, st);
+    if (b->vals) cudaFreeAsync(b->vals, st);
+    if (st) cudaStreamSynchronize(st);
     delete b;
 }
 
@@ -712,6 +760,8 @@ void sdnn_net_destroy(sdnn_net* net) {
     cudaFree(net->n_sel);
     cudaFree(net->cub_tmp);
     if (net->pinned) cudaFreeHost(net->pinned);
+    for (auto e : net->stage_ev)
+        if (e) cudaEventDestroy(e);
     if (net->ev0) cudaEventDestroy(net->ev0);
     if (net->ev1) cudaEventDestroy(net->ev1);
     if (net->stream) cudaStreamDestroy(net->stream);
@@ -774,6 +824,12 @@ int sdnn_net_weight_bytes(const sdnn_net* net, int64_t* bytes) {
     int64_t s = 0;
     for (auto& L : net->layers) s += L.bytes;
     *bytes = s;
+    return SDNN_OK;
+}
+
+int sdnn_batch_h2d_bytes(const sdnn_batch* b, int64_t* bytes) {
+    if (!b || !bytes) return fail(SDNN_ERR_PARAMETER, "null argument");
+    *bytes = b->h2d_bytes;
     return SDNN_OK;
 }
 
@@ -954,8 +1010,13 @@ int sdnn_bias_relu_clamp(int device, int dtype, int64_t n_rows, int64_t n_cols, 
     if (!out || n_rows < 0 || n_cols < 1) return fail(SDNN_ERR_PARAMETER, "bad shape");
     sdnn_net* net = nullptr;
     if (int rc = make_net(device, dtype, n_cols, &net)) return rc;
-    sdnn_batch* b = nullptr;
-    int rc = sdnn_batch_upload(net, n_rows, off, cols, vals, &b);
+    sdnn_batch* b = new sdnn_batch;
+    b->net = net;
+    static const int64_t zero_off[1] = {0};
+    const int64_t* yo = n_rows > 0 ? off : zero_off;
+    // raw upload: int32 columns and every value, as the CSR kernels need
+    int rc = dtype == SDNN_F64 ? upload_csr<double>(net, n_rows, yo, cols, vals, n_cols, b, true)
+                               : upload_csr<float>(net, n_rows, yo, cols, vals, n_cols, b, true);
     sdnn_result* res = nullptr;
     if (!rc) {
         res = new sdnn_result;
@@ -987,7 +1048,8 @@ int sdnn_bias_relu_clamp(int device, int dtype, int64_t n_rows, int64_t n_cols, 
             CK(cudaMemcpyAsync(pos, res->off.data(), n_rows * 8, cudaMemcpyHostToDevice, net->stream));
             CK(cudaMalloc(&oc, std::max<int64_t>(total, 1) * 4));
             CK(cudaMalloc(&ov, std::max<int64_t>(total, 1) * sizeof(T)));
-            csr_brc_write_kernel<T><<<grid, 256, 0, net->stream>>>(b->off, b->cols, reinterpret_cast<const T*>(b->vals),
+            csr_brc_write_kernel<T><<<grid, 256, 0, net->stream>>>(b->off, reinterpret_cast<const int32_t*>(b->cols),
+                                                                   reinterpret_cast<const T*>(b->vals),
                                                                    n_rows, (T)bias, (T)ymax, pos, oc, ov);
             CK(cudaGetLastError());
             std::vector<int32_t> hc(total);
@@ -1008,7 +1070,7 @@ int sdnn_bias_relu_clamp(int device, int dtype, int64_t n_rows, int64_t n_cols, 
         };
         rc = dtype == SDNN_F64 ? body(double{}) : body(float{});
     }
-    if (b) sdnn_batch_free(b);
+    if (b) free_batch(b);
     sdnn_net_destroy(net);
     if (rc) {
         delete res;

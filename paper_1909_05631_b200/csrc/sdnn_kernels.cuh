@@ -212,9 +212,16 @@ __device__ __forceinline__ void publish_alive(uint32_t* aw, unsigned bits, int32
 // zeroes the tile's zero line in both slab buffers.
 constexpr int kDensifyThreads = 512;
 
+// Columns arrive as uint16 (col_bytes 2, n_in <= 65536) or int32; a null
+// value array means every stored value is 1.0 (binary images).
+__device__ __forceinline__ int load_col(const void* cols, int col_bytes, int64_t q) {
+    return col_bytes == 2 ? (int)__ldg(reinterpret_cast<const unsigned short*>(cols) + q)
+                          : __ldg(reinterpret_cast<const int*>(cols) + q);
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kDensifyThreads) densify_kernel(const int64_t* __restrict__ csr_off,
-                                                                  const int32_t* __restrict__ csr_cols,
+                                                                  const void* __restrict__ csr_cols, int col_bytes,
                                                                   const T* __restrict__ csr_vals,
                                                                   const int32_t* __restrict__ rowid, int n_in,
                                                                   int ld, int n_tiles, int kc, T* slab0,
@@ -254,8 +261,8 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_kernel(const int64_t*
         for (int i = 0; i < RW; ++i) {
             const int r = warp + i * NW;
             const int64_t q = s_pos[r] + lane;
-            cb[i] = q < s_end[r] ? csr_cols[q] : INT32_MAX;
-            vb[i] = q < s_end[r] ? csr_vals[q] : T(0);
+            cb[i] = q < s_end[r] ? load_col(csr_cols, col_bytes, q) : INT32_MAX;
+            vb[i] = q < s_end[r] ? (csr_vals ? csr_vals[q] : T(1)) : T(0);
         }
         char* s0 = reinterpret_cast<char*>(slab0 + (size_t)t * ld * TR);
         uint2* gm = meta0 + (size_t)t * ld;
@@ -283,8 +290,8 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_kernel(const int64_t*
                     if (lane == 0) s_pos[r] = base;
                     __syncwarp();  // the new base is visible to later reads
                     const int64_t q = base + lane;
-                    cb[i] = q < s_end[r] ? csr_cols[q] : INT32_MAX;
-                    vb[i] = q < s_end[r] ? csr_vals[q] : T(0);
+                    cb[i] = q < s_end[r] ? load_col(csr_cols, col_bytes, q) : INT32_MAX;
+                    vb[i] = q < s_end[r] ? (csr_vals ? csr_vals[q] : T(1)) : T(0);
                 }
             }
             __syncthreads();

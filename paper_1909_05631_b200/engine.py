@@ -162,6 +162,9 @@ class DeviceBatch:
             net.handle, self.n_rows, _lib.ptr(_nonempty(off, np.int64)),
             _lib.ptr(_nonempty(cols, np.int64)), _lib.ptr(_nonempty(vals, np.float64)),
             ctypes.byref(self.handle)))
+        b = ctypes.c_int64()
+        _lib.check(_lib.lib().sdnn_batch_h2d_bytes(self.handle, ctypes.byref(b)))
+        self.h2d_bytes = b.value
 
     def close(self):
         if self.handle:
