@@ -184,10 +184,11 @@ def run_ours(args, dist: RankGroup):
     r0, r1 = shard(w.batch, dist.rank, dist.world)
     rows = r1 - r0
     elem = 8 if args.dtype == "f64" else 4
+    threads = host_threads()
     t_setup = time.perf_counter()
     net = DeviceNetwork(w.n, dev, args.dtype)
-    net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias)
-    off, cols, vals = W.images(w, n_rows=rows, row0=r0)
+    net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias, threads=threads)
+    off, cols, vals = W.images(w, n_rows=rows, row0=r0, threads=threads)
     nnz0 = int(off[-1])
     batch = net.upload_csr(rows, off, cols, vals)
     setup_s = time.perf_counter() - t_setup
@@ -390,6 +391,12 @@ def run_reference(args, dist: RankGroup):
     }
 
 
+def host_threads() -> int:
+    """Host threads per rank: the node's cores split over its local ranks."""
+    local = max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
+    return max(1, (os.cpu_count() or 1) // local)
+
+
 def workload(args) -> W.Workload:
     w = W.CONFIGS[args.workload]
     kw = {}
@@ -418,6 +425,7 @@ def main(argv=None):
     ap.add_argument("--companions", default="K2:120",
                     help="comma list NAME[:LAYERS] of live companions ('' to skip)")
     args = ap.parse_args(argv)
+    os.environ.setdefault("OMP_NUM_THREADS", str(host_threads()))  # libsdnn's upload threads
     dist = RankGroup()
     try:
         line = run_reference(args, dist) if args.impl == "reference" else run_ours(args, dist)

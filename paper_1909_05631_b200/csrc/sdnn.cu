@@ -469,15 +469,14 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     const void* dfn = (const void*)densify_kernel<T>;
     CK(cudaFuncSetAttribute(dfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
     // gather pipeline: 1 = register double-buffered 4-line sub-batches
-    // (default), 2 = (2 lines, double-buffered), 3 = (4 lines, single),
-    // 4 = per-warp TMA line rings
+    // (default), 2 = (2 lines, double-buffered), 3 = (4 lines, single).
+    // (A per-warp TMA bulk-copy ring was measured 1.5x slower: one bulk
+    // copy per <= 1 KB line is below the TMA unit's efficient size.)
     const int kvar = env_int("SDNN_KVAR", 1);
-    const void* fn = kvar == 2   ? (const void*)net_kernel<T, 2, 1>
-                     : kvar == 3 ? (const void*)net_kernel<T, 4, 0>
-                     : kvar == 4 ? (const void*)net_kernel<T, 4, 2>
-                                 : (const void*)net_kernel<T, 4, 1>;
-    const size_t ring_bytes = kvar == 4 ? (size_t)kWarps * kRing * kLineBytes : 0;
-    const size_t smem = ring_bytes + (size_t)tiles1 * 4;
+    const void* fn = kvar == 2   ? (const void*)net_kernel<T, 2, true>
+                     : kvar == 3 ? (const void*)net_kernel<T, 4, false>
+                                 : (const void*)net_kernel<T, 4, true>;
+    const size_t smem = (size_t)tiles1 * 4;
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem));

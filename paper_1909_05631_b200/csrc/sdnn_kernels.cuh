@@ -163,40 +163,6 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
-// ---- TMA bulk copies + mbarriers (per-warp line rings) --------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* m, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* m, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* m, unsigned parity) {
-    uint32_t done;
-    do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(smem_u32(m)), "r"(parity)
-            : "memory");
-    } while (!done);
-}
-// global -> shared bulk copy (TMA), completion counted on the mbarrier
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* m) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(m))
-                 : "memory");
-}
-// order this thread's earlier generic-proxy shared accesses before later
-// async-proxy (TMA) writes to the same buffer
-__device__ __forceinline__ void fence_proxy_async_smem() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
 // Sense-reversing grid barrier for a cooperative launch (all CTAs resident).
 // The gpu-scope fences make every layer's stores visible to the next layer
 // and invalidate this SM's L1, so plain (L1-cached) loads are coherent.
@@ -366,19 +332,9 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_kernel(const int64_t*
 // multiple of GB with zero-line, zero-weight entries), which is then
 // gathered GB lines at a time, double-buffered when DBUF.  Each lane chains
 // its RPL rows separately; one 256-bit load per lane per line.
-// Per-warp TMA ring: S line buffers of kLineBytes plus their mbarriers, and
-// the running count of bulk copies issued through it (parity tracking).
-constexpr int kRing = 8;
-struct WarpRing {
-    unsigned char* buf;  // [kRing][kLineBytes]
-    uint64_t* bar;       // [kRing]
-    unsigned issued;     // copies issued so far (uniform across the warp)
-};
-
-template <typename T, int GB, int MODE>
+template <typename T, int GB, bool DBUF>
 __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<T>& L, int l, int t,
-                                           int j0, int j1, SlotEntry<T>* wlist, WarpRing& ring) {
-    constexpr bool DBUF = MODE == 1;
+                                           int j0, int j1, SlotEntry<T>* wlist) {
     using A = Arith<T>;
     constexpr int RPL = rows_per_lane<T>(), AW = alive_words<T>();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -468,48 +424,7 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
                 for (int c = 0; c < RPL; ++c) acc[c] = A::muladd(y[u][c], w, acc[c]);
             }
         };
-        if (MODE == 2) {
-            // TMA ring: lane 0 streams each live line (its kept sectors,
-            // contiguous in the heap) into the warp's ring, kRing lines
-            // ahead; every lane then reads its own sector from shared memory
-            const unsigned e0 = ring.issued;
-            auto produce = [&](int i) {
-                const SlotEntry<T> e = wlist[i];
-                const unsigned slot = (e0 + i) % kRing;
-                const unsigned bytes = (unsigned)__popc(e.mask) * 32u;
-                fence_proxy_async_smem();
-                mbar_expect_tx(&ring.bar[slot], bytes);
-                bulk_g2s(ring.buf + slot * kLineBytes, in + (size_t)e.base * 32, bytes, &ring.bar[slot]);
-            };
-            if (lane == 0)
-                for (int i = 0; i < min(n, kRing); ++i) produce(i);
-            for (int i = 0; i < n; ++i) {
-                const unsigned slot = (e0 + i) % kRing;
-                mbar_wait(&ring.bar[slot], ((e0 + i) / kRing) & 1u);
-                const SlotEntry<T> e = wlist[i];
-                T y[RPL];
-                if (e.mask & lbit) {
-                    const uint4* src = reinterpret_cast<const uint4*>(ring.buf + slot * kLineBytes +
-                                                                      __popc(e.mask & below) * 32);
-                    const uint4 q0 = src[0], q1 = src[1];
-                    const T* qv0 = reinterpret_cast<const T*>(&q0);
-                    const T* qv1 = reinterpret_cast<const T*>(&q1);
-#pragma unroll
-                    for (int c = 0; c < RPL / 2; ++c) {
-                        y[c] = qv0[c];
-                        y[c + RPL / 2] = qv1[c];
-                    }
-                } else {
-#pragma unroll
-                    for (int c = 0; c < RPL; ++c) y[c] = T(0);
-                }
-#pragma unroll
-                for (int c = 0; c < RPL; ++c) acc[c] = A::muladd(y[c], e.w, acc[c]);
-                __syncwarp();  // every lane is done with this ring slot
-                if (lane == 0 && i + kRing < n) produce(i + kRing);
-            }
-            ring.issued = e0 + n;
-        } else if (DBUF) {
+        if (DBUF) {
             // the next sub-batch's loads are in flight while this one is consumed
             T ya[GB][RPL], yb[GB][RPL];
             if (npad) issue(ya, 0);
@@ -558,14 +473,11 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
 }
 
 // GB = lines gathered per sub-batch per warp.
-template <typename T, int GB, int MODE>
-__global__ void __launch_bounds__(kThreads, MODE == 2 ? 3 : ((MODE == 1 ? 2 * GB : GB) * 8 <= 32 ? 3 : 2))
+template <typename T, int GB, bool DBUF>
+__global__ void __launch_bounds__(kThreads, (DBUF ? 2 * GB : GB) * 8 <= 32 ? 3 : 2)  // y registers
     net_kernel(NetArgs<T> a) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    // [0, ring bytes): per-warp TMA rings (MODE 2); then the live-tile list
-    constexpr size_t kRingBytes = MODE == 2 ? (size_t)kWarps * kRing * kLineBytes : 0;
-    int32_t* tiles = reinterpret_cast<int32_t*>(smem + kRingBytes);
-    __shared__ uint64_t s_bar[kWarps][kRing];
+    extern __shared__ __align__(16) unsigned char smem[];
+    int32_t* tiles = reinterpret_cast<int32_t*>(smem);
     __shared__ SlotEntry<T> s_list[kWarps][32];
     __shared__ int s_count;
     __shared__ int s_scan[kWarps + 1];
@@ -574,12 +486,6 @@ __global__ void __launch_bounds__(kThreads, MODE == 2 ? 3 : ((MODE == 1 ? 2 * GB
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned nb = gridDim.x;
     if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[0] = globaltimer();
-    WarpRing ring{smem + (size_t)warp * kRing * kLineBytes, s_bar[warp], 0u};
-    if (MODE == 2) {
-        if (lane < kRing) mbar_init(&s_bar[warp][lane], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        __syncwarp();
-    }
 
     bool all_dead = false;
     for (int l = 0; l < a.L; ++l) {
@@ -627,7 +533,7 @@ __global__ void __launch_bounds__(kThreads, MODE == 2 ? 3 : ((MODE == 1 ? 2 * GB
             const int t = tiles[it / nblk];
             const int bb = (int)(it % nblk);
             const int j0 = bb * a.jb, j1 = min(a.n_out, j0 + a.jb);
-            layer_item<T, GB, MODE>(a, L, l, t, j0, j1, s_list[warp], ring);
+            layer_item<T, GB, DBUF>(a, L, l, t, j0, j1, s_list[warp]);
         }
         grid_barrier(a.bar, nb);
         if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[l + 1] = globaltimer();
