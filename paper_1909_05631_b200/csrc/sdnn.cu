@@ -100,7 +100,7 @@ struct sdnn_net {
     int64_t n = 0;
     int elem = 4;
     int sm_count = 0;
-    int jb = 512;  // outputs per work item
+    int jb = 256;  // outputs per work item
     std::vector<DevLayer> layers;
     void* descs = nullptr;  // device LayerDesc<T>[layers]
     int64_t descs_n = 0;    // layers mirrored in `descs`

@@ -275,23 +275,31 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_kernel(const int64_t*
                 for (int k = tid; k < kn; k += blockDim.x) gm[k0 + k] = make_uint2(0u, 0u);
                 continue;
             }
+            // rounds: drop every window's in-chunk entries into the staging
+            // tile, then refill all exhausted windows at once (their loads
+            // overlap); repeat while a refill happened
+            for (bool refilled = true; refilled;) {
+                refilled = false;
 #pragma unroll
-            for (int i = 0; i < RW; ++i) {
-                const int r = warp + i * NW;
-                while (true) {
+                for (int i = 0; i < RW; ++i) {
                     if (cb[i] < k0 + kn) {
-                        stage[(size_t)(cb[i] - k0) * TR + r] = vb[i];
+                        stage[(size_t)(cb[i] - k0) * TR + warp + i * NW] = vb[i];
                         cb[i] = INT32_MAX;
                     }
-                    if (__ballot_sync(0xffffffffu, cb[i] != INT32_MAX)) break;  // window not used up
+                }
+#pragma unroll
+                for (int i = 0; i < RW; ++i) {
+                    const int r = warp + i * NW;
+                    if (__any_sync(0xffffffffu, cb[i] != INT32_MAX)) continue;  // window not used up
                     const int64_t base = s_pos[r] + 32;
-                    if (base >= s_end[r]) break;                              // row done
+                    if (base >= s_end[r]) continue;                             // row done
                     __syncwarp();  // every lane has read s_pos[r]
                     if (lane == 0) s_pos[r] = base;
-                    __syncwarp();  // the new base is visible to later reads
+                    __syncwarp();
                     const int64_t q = base + lane;
                     cb[i] = q < s_end[r] ? load_col(csr_cols, col_bytes, q) : INT32_MAX;
                     vb[i] = q < s_end[r] ? (csr_vals ? csr_vals[q] : T(1)) : T(0);
+                    refilled = true;
                 }
             }
             __syncthreads();
