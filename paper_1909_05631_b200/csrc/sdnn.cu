@@ -464,7 +464,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     a.work = work;
     a.stamps = net->layer_timing ? stamps : nullptr;
     a.jb = env_int("SDNN_JB", net->jb);
-    const int kc = env_int("SDNN_DENSIFY_KC", 96);  // input neurons per staging chunk
+    const int kc = std::min(1024, env_int("SDNN_DENSIFY_KC", 96));  // input neurons per staging chunk
     const size_t dsmem = (size_t)kc * kLineBytes;
     const void* dfn = (const void*)densify_kernel<T>;
     CK(cudaFuncSetAttribute(dfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
@@ -486,10 +486,16 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     void* args[] = {(void*)&a};
     CK(cudaEventRecord(net->ev0, net->stream));
     if (n_tiles) {
-        const int dgrid = (int)std::min<int64_t>(n_tiles, (int64_t)net->sm_count * 4);
+        // lines densify does not touch stay {mask 0}: zero the meta first
+        CK(cudaMemsetAsync(a.meta[0], 0, (size_t)n_tiles * ld * sizeof(uint2), net->stream));
+        // each tile's neurons are split into spans handled by separate blocks
+        const int spans = std::max(1, env_int("SDNN_DENSIFY_SPANS", 16));
+        const int span = (int)(((n_in + spans - 1) / spans + kc - 1) / kc * kc);
+        const int64_t blocks = n_tiles * ((n_in + span - 1) / span);
+        const int dgrid = (int)std::min<int64_t>(blocks, (int64_t)net->sm_count * 32);
         densify_kernel<T><<<dgrid, kDensifyThreads, dsmem, net->stream>>>(
             batch->off, batch->cols, batch->col_bytes, reinterpret_cast<const T*>(batch->vals), net->rowid,
-            (int)n_in, (int)ld, (int)n_tiles, kc, a.slab[0], a.meta[0], heap, net->alive, tile_count);
+            (int)n_in, (int)ld, (int)n_tiles, kc, span, a.slab[0], a.meta[0], heap, net->alive, tile_count);
         CK(cudaGetLastError());
         res->launches += 1;
     }

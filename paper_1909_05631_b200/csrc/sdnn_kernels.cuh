@@ -224,35 +224,46 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_kernel(const int64_t*
                                                                   const void* __restrict__ csr_cols, int col_bytes,
                                                                   const T* __restrict__ csr_vals,
                                                                   const int32_t* __restrict__ rowid, int n_in,
-                                                                  int ld, int n_tiles, int kc, T* slab0,
+                                                                  int ld, int n_tiles, int kc, int span, T* slab0,
                                                                   uint2* meta0, uint32_t* heap0, uint32_t* alive0,
                                                                   int32_t* tile_count0) {
     extern __shared__ __align__(16) unsigned char dsm[];
-    constexpr int TR = tile_rows<T>(), AW = alive_words<T>();
+    constexpr int TR = tile_rows<T>(), AW = alive_words<T>(), RPL = rows_per_lane<T>();
     constexpr int NW = kDensifyThreads / 32, RW = TR / NW;  // rows per warp
     T* stage = reinterpret_cast<T*>(dsm);                  // [kc][TR]
     __shared__ int64_t s_pos[TR], s_end[TR];               // window base, row end
     __shared__ uint32_t s_alive[AW];
-    __shared__ unsigned s_heap;                            // sectors used so far
+    __shared__ uint32_t s_live[32];                        // chunk lines touched (kc <= 1024)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
     {
         uint4* st4 = reinterpret_cast<uint4*>(stage);
         for (int i = tid; i < kc * kLineBytes / 16; i += blockDim.x) st4[i] = z4;
+        if (tid < 32) s_live[tid] = 0u;
     }
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    // block b: tile b / n_spans, input neurons [kbeg, kend) of that tile
+    const int n_spans = (n_in + span - 1) / span;
+    for (int bb = blockIdx.x; bb < n_tiles * n_spans; bb += gridDim.x) {
+        const int t = bb / n_spans;
+        const int kbeg = (bb % n_spans) * span, kend = min(n_in, kbeg + span);
         if (tid < AW) s_alive[tid] = 0u;
-        if (tid == 0) s_heap = 0u;
         __syncthreads();
         for (int r = tid; r < TR; r += blockDim.x) {
             const int row = rowid[(size_t)t * TR + r];
-            const int64_t p = row >= 0 ? csr_off[row] : 0, e = row >= 0 ? csr_off[row + 1] : 0;
-            s_pos[r] = p;
-            s_end[r] = e;
-            if (e > p) {
+            int64_t p = row >= 0 ? csr_off[row] : 0, e = row >= 0 ? csr_off[row + 1] : 0;
+            if (e > p) {  // a row with an entry anywhere is live
                 atomicOr(&s_alive[r / 32], 1u << (r % 32));
                 atomicOr(&s_alive[AW - 1], 1u);
             }
+            // first entry at or after kbeg (columns ascend)
+            int64_t lo = p, hi = e;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (load_col(csr_cols, col_bytes, mid) < kbeg) lo = mid + 1;
+                else hi = mid;
+            }
+            s_pos[r] = lo;
+            s_end[r] = e;
         }
         __syncthreads();
         int cb[RW];
@@ -266,15 +277,12 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_kernel(const int64_t*
         }
         char* s0 = reinterpret_cast<char*>(slab0 + (size_t)t * ld * TR);
         uint2* gm = meta0 + (size_t)t * ld;
-        for (int k0 = 0; k0 < n_in; k0 += kc) {
-            const int kn = min(kc, n_in - k0);
+        for (int k0 = kbeg; k0 < kend; k0 += kc) {
+            const int kn = min(kc, kend - k0);
             bool mine = false;
 #pragma unroll
             for (int i = 0; i < RW; ++i) mine |= cb[i] < k0 + kn;
-            if (!__syncthreads_or(mine)) {  // the whole chunk is zero for every row
-                for (int k = tid; k < kn; k += blockDim.x) gm[k0 + k] = make_uint2(0u, 0u);
-                continue;
-            }
+            if (!__syncthreads_or(mine)) continue;  // the whole chunk is zero for every row
             // rounds: drop every window's in-chunk entries into the staging
             // tile, then refill all exhausted windows at once (their loads
             // overlap); repeat while a refill happened
@@ -283,7 +291,11 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_kernel(const int64_t*
 #pragma unroll
                 for (int i = 0; i < RW; ++i) {
                     if (cb[i] < k0 + kn) {
-                        stage[(size_t)(cb[i] - k0) * TR + warp + i * NW] = vb[i];
+                        const int kk = cb[i] - k0, r = warp + i * NW;
+                        // sector of row r sits at position (r / RPL) ^ (kk & 31): rows of one
+                        // warp row-window hit different banks, line reads stay conflict-free
+                        stage[(size_t)kk * TR + (((r / RPL) ^ (kk & 31)) * RPL) + r % RPL] = vb[i];
+                        atomicOr(&s_live[kk >> 5], 1u << (kk & 31));
                         cb[i] = INT32_MAX;
                     }
                 }
@@ -304,8 +316,11 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_kernel(const int64_t*
             }
             __syncthreads();
             // write out the chunk's nonzero lines and their sector masks
+            // (lines no row touched keep the zero meta set before the launch)
             for (int k = warp; k < kn; k += NW) {
-                uint4* src = reinterpret_cast<uint4*>(reinterpret_cast<char*>(stage) + (size_t)k * kLineBytes + lane * 32);
+                if (!((s_live[k >> 5] >> (k & 31)) & 1u)) continue;
+                uint4* src = reinterpret_cast<uint4*>(reinterpret_cast<char*>(stage) + (size_t)k * kLineBytes +
+                                                      ((lane ^ (k & 31)) * 32));
                 const uint4 a = src[0], b = src[1];
                 const T* sv = reinterpret_cast<const T*>(src);
                 bool any = false;
@@ -313,20 +328,20 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_kernel(const int64_t*
                 for (int c = 0; c < rows_per_lane<T>(); ++c) any |= sv[c] != T(0);
                 const unsigned m = __ballot_sync(0xffffffffu, any);
                 unsigned base = 0u;
-                if (lane == 0 && m) base = atomicAdd(&s_heap, (unsigned)__popc(m));
+                if (lane == 0 && m) base = atomicAdd(&heap0[t], (unsigned)__popc(m));
                 base = __shfl_sync(0xffffffffu, base, 0);
                 if (any) st32_bits(s0 + (size_t)(base + __popc(m & ((1u << lane) - 1u))) * 32, a, b);
                 if (lane == 0) gm[k0 + k] = make_uint2(m, base);
                 src[0] = z4;  // re-zero for the next chunk
                 src[1] = z4;
             }
+            __syncthreads();
+            for (int i = tid; i < (kc + 31) / 32; i += blockDim.x) s_live[i] = 0u;
         }
         __syncthreads();
-        if (tid < AW) alive0[(size_t)t * AW + tid] = s_alive[tid];
-        if (tid == 0) {
-            heap0[t] = s_heap;
-            if (s_alive[AW - 1]) atomicAdd(tile_count0, 1);
-        }
+        if (tid < AW - 1 && s_alive[tid]) atomicOr(&alive0[(size_t)t * AW + tid], s_alive[tid]);
+        if (tid == AW - 1 && s_alive[tid] && atomicOr(&alive0[(size_t)t * AW + tid], 1u) == 0u)
+            atomicAdd(tile_count0, 1);
     }
 }
 
