@@ -117,6 +117,29 @@ __device__ __forceinline__ void st32_bits(char* p, const uint4& a, const uint4& 
                  : "memory");
 }
 
+// Weight loads carry an L2 evict-last hint: every tile of a layer re-reads
+// the layer's weights, so they should outlive the streamed activation lines.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ int ld_w(const int32_t* p, uint64_t pol) {
+    int v;
+    asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float ld_w(const float* p, uint64_t pol) {
+    float v;
+    asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double ld_w(const double* p, uint64_t pol) {
+    double v;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
 // One live slot of a warp's compacted slot list (16 bytes).
 template <typename T>
 struct __align__(16) SlotEntry {
@@ -388,13 +411,14 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
         return (size_t)j * L.wp + (size_t)(b % nb) * 32 + lane;
     };
     // pipeline registers: (k1, w1) for batch b+1, (k2, w2) for batch b+2
-    int k0 = __ldg(L.idx + slot_ptr(0));
-    T w0 = __ldg(L.val + slot_ptr(0));
+    const uint64_t wpol = policy_evict_last();
+    int k0 = ld_w(L.idx + slot_ptr(0), wpol);
+    T w0 = ld_w(L.val + slot_ptr(0), wpol);
     int k1 = -1, k2 = -1;
     T w1 = T(0), w2 = T(0);
     if (total > 1) {
-        k1 = __ldg(L.idx + slot_ptr(1));
-        w1 = __ldg(L.val + slot_ptr(1));
+        k1 = ld_w(L.idx + slot_ptr(1), wpol);
+        w1 = ld_w(L.val + slot_ptr(1), wpol);
     }
     uint2 m0 = k0 >= 0 ? imeta[k0] : make_uint2(0u, 0u);
     T acc[RPL];
@@ -404,8 +428,8 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
     for (int b = 0; b < total; ++b) {
         // issue the next loads before working on batch b
         if (b + 2 < total) {
-            k2 = __ldg(L.idx + slot_ptr(b + 2));
-            w2 = __ldg(L.val + slot_ptr(b + 2));
+            k2 = ld_w(L.idx + slot_ptr(b + 2), wpol);
+            w2 = ld_w(L.val + slot_ptr(b + 2), wpol);
         }
         const uint2 m1 = (b + 1 < total && k1 >= 0) ? imeta[k1] : make_uint2(0u, 0u);
 
