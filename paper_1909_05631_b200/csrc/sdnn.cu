@@ -472,10 +472,14 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     // (default), 2 = (2 lines, double-buffered), 3 = (4 lines, single).
     // (A per-warp TMA bulk-copy ring was measured 1.5x slower: one bulk
     // copy per <= 1 KB line is below the TMA unit's efficient size.)
+    // dead sectors: 1 = predicated off, no request (default; the L1 data path
+    // is the limit for sparse lines), 0 = read the shared zero sector
     const int kvar = env_int("SDNN_KVAR", 1);
-    const void* fn = kvar == 2   ? (const void*)net_kernel<T, 2, true>
-                     : kvar == 3 ? (const void*)net_kernel<T, 4, false>
-                                 : (const void*)net_kernel<T, 4, true>;
+    const int pred_loads = env_int("SDNN_PRED", 1);
+    const void* fn = kvar == 2   ? (const void*)net_kernel<T, 2, true, false>
+                     : kvar == 3 ? (const void*)net_kernel<T, 4, false, false>
+                     : pred_loads ? (const void*)net_kernel<T, 4, true, true>
+                                  : (const void*)net_kernel<T, 4, true, false>;
     const size_t smem = (size_t)tiles1 * 4;
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
