@@ -98,6 +98,24 @@ __device__ __forceinline__ void ld32(float (&d)[8], const char* p) {
 __device__ __forceinline__ void ld32(double (&d)[4], const char* p) {
     asm("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(d[0]), "=d"(d[1]), "=d"(d[2]), "=d"(d[3]) : "l"(p));
 }
+// Predicated 256-bit gather: zeros without any memory request when the
+// lane's sector is not live.
+__device__ __forceinline__ void ld32_pred(float (&d)[8], const char* p, bool live) {
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %9, 0;\n\t"
+        "mov.b32 %0, 0;\n\tmov.b32 %1, 0;\n\tmov.b32 %2, 0;\n\tmov.b32 %3, 0;\n\t"
+        "mov.b32 %4, 0;\n\tmov.b32 %5, 0;\n\tmov.b32 %6, 0;\n\tmov.b32 %7, 0;\n\t"
+        "@q ld.global.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n\t}"
+        : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3]), "=f"(d[4]), "=f"(d[5]), "=f"(d[6]), "=f"(d[7])
+        : "l"(p), "r"((unsigned)live));
+}
+__device__ __forceinline__ void ld32_pred(double (&d)[4], const char* p, bool live) {
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t"
+        "mov.b64 %0, 0;\n\tmov.b64 %1, 0;\n\tmov.b64 %2, 0;\n\tmov.b64 %3, 0;\n\t"
+        "@q ld.global.v4.f64 {%0, %1, %2, %3}, [%4];\n\t}"
+        : "=d"(d[0]), "=d"(d[1]), "=d"(d[2]), "=d"(d[3])
+        : "l"(p), "r"((unsigned)live));
+}
+
 // Output lines are streamed (evict-first): a layer's output is read only in
 // the next layer, after the whole slab has been written, so keeping it in L2
 // would only push out the input lines still being gathered.
@@ -378,7 +396,7 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_kernel(const int64_t*
 // multiple of GB with zero-line, zero-weight entries), which is then
 // gathered GB lines at a time, double-buffered when DBUF.  Each lane chains
 // its RPL rows separately; one 256-bit load per lane per line.
-template <typename T, int GB, bool DBUF>
+template <typename T, int GB, bool DBUF, bool PRED>
 __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<T>& L, int l, int t,
                                            int j0, int j1, SlotEntry<T>* wlist) {
     using A = Arith<T>;
@@ -460,7 +478,10 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
 #pragma unroll
             for (int u = 0; u < GB; ++u) {
                 const SlotEntry<T> e = wlist[i0 + u];
-                ld32(y[u], (e.mask & lbit) ? in + (size_t)(e.base + __popc(e.mask & below)) * 32 : zsec);
+                if (PRED)  // dead lanes: no request, zeros (adding +-0 never changes a chain)
+                    ld32_pred(y[u], in + (size_t)(e.base + __popc(e.mask & below)) * 32, (e.mask & lbit) != 0u);
+                else       // dead lanes read the shared zero sector (an L1 hit)
+                    ld32(y[u], (e.mask & lbit) ? in + (size_t)(e.base + __popc(e.mask & below)) * 32 : zsec);
             }
         };
         auto consume = [&](const T (&y)[GB][RPL], int i0) {
@@ -520,7 +541,7 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
 }
 
 // GB = lines gathered per sub-batch per warp.
-template <typename T, int GB, bool DBUF>
+template <typename T, int GB, bool DBUF, bool PRED>
 __global__ void __launch_bounds__(kThreads, (DBUF ? 2 * GB : GB) * 8 <= 32 ? 3 : 2)  // y registers
     net_kernel(NetArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -580,7 +601,7 @@ __global__ void __launch_bounds__(kThreads, (DBUF ? 2 * GB : GB) * 8 <= 32 ? 3 :
             const int t = tiles[it / nblk];
             const int bb = (int)(it % nblk);
             const int j0 = bb * a.jb, j1 = min(a.n_out, j0 + a.jb);
-            layer_item<T, GB, DBUF>(a, L, l, t, j0, j1, s_list[warp]);
+            layer_item<T, GB, DBUF, PRED>(a, L, l, t, j0, j1, s_list[warp]);
         }
         grid_barrier(a.bar, nb);
         if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[l + 1] = globaltimer();
