@@ -494,12 +494,27 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
         CK(cudaMemsetAsync(a.meta[0], 0, (size_t)n_tiles * ld * sizeof(uint2), net->stream));
         // each tile's neurons are split into spans handled by separate blocks
         const int spans = std::max(1, env_int("SDNN_DENSIFY_SPANS", 16));
-        const int span = (int)(((n_in + spans - 1) / spans + kc - 1) / kc * kc);
-        const int64_t blocks = n_tiles * ((n_in + span - 1) / span);
-        const int dgrid = (int)std::min<int64_t>(blocks, (int64_t)net->sm_count * 32);
-        densify_kernel<T><<<dgrid, kDensifyThreads, dsmem, net->stream>>>(
-            batch->off, batch->cols, batch->col_bytes, reinterpret_cast<const T*>(batch->vals), net->rowid,
-            (int)n_in, (int)ld, (int)n_tiles, kc, span, a.slab[0], a.meta[0], heap, net->alive, tile_count);
+        const bool bin = batch->vals == nullptr && env_int("SDNN_BIN", 1) != 0;
+        a.bin_in = bin ? 1 : 0;
+        if (bin) {  // binary Y0: bit-line tiles
+            const int kcb = 1024;
+            const int span = (int)(((n_in + spans - 1) / spans + kcb - 1) / kcb * kcb);
+            const int64_t blocks = n_tiles * ((n_in + span - 1) / span);
+            const int dgrid = (int)std::min<int64_t>(blocks, (int64_t)net->sm_count * 32);
+            const size_t bsmem = (size_t)kcb * (TR / 32) * 4;
+            CK(cudaFuncSetAttribute((const void*)densify_bin_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)bsmem));
+            densify_bin_kernel<T><<<dgrid, kDensifyThreads, bsmem, net->stream>>>(
+                batch->off, batch->cols, batch->col_bytes, net->rowid, (int)n_in, (int)ld, (int)n_tiles, kcb, span,
+                a.slab[0], a.meta[0], heap, net->alive, tile_count);
+        } else {
+            const int span = (int)(((n_in + spans - 1) / spans + kc - 1) / kc * kc);
+            const int64_t blocks = n_tiles * ((n_in + span - 1) / span);
+            const int dgrid = (int)std::min<int64_t>(blocks, (int64_t)net->sm_count * 32);
+            densify_kernel<T><<<dgrid, kDensifyThreads, dsmem, net->stream>>>(
+                batch->off, batch->cols, batch->col_bytes, reinterpret_cast<const T*>(batch->vals), net->rowid,
+                (int)n_in, (int)ld, (int)n_tiles, kc, span, a.slab[0], a.meta[0], heap, net->alive, tile_count);
+        }
         CK(cudaGetLastError());
         res->launches += 1;
     }

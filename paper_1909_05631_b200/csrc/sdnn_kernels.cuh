@@ -193,6 +193,7 @@ struct NetArgs {
     unsigned* work;       // [L] per-layer work-item counters (zeroed)
     unsigned long long* stamps;  // [L + 1] globaltimer after each layer, or null
     int jb;               // outputs per work item
+    int bin_in;           // layer-0 input is bit-lines (binary Y0)
 };
 
 constexpr int kThreads = 256;
@@ -386,6 +387,118 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_kernel(const int64_t*
     }
 }
 
+// Binary Y0 (every stored value 1.0, the challenge's thresholded images):
+// tiles of bit-lines, one 32-byte line of TR bits per (tile, neuron), bit r
+// for row r.  Same spans / row cursors as densify_kernel; a chunk of kc
+// lines is assembled in shared memory with atomicOr, then each nonzero line
+// is appended to the tile's heap (one 32-byte unit) with meta {all lanes,
+// heap index}.  Layer 1 then reads 32 bytes per gathered line instead of 1 KB.
+template <typename T>
+__global__ void __launch_bounds__(kDensifyThreads) densify_bin_kernel(const int64_t* __restrict__ csr_off,
+                                                                      const void* __restrict__ csr_cols,
+                                                                      int col_bytes,
+                                                                      const int32_t* __restrict__ rowid, int n_in,
+                                                                      int ld, int n_tiles, int kc, int span,
+                                                                      T* slab0, uint2* meta0, uint32_t* heap0,
+                                                                      uint32_t* alive0, int32_t* tile_count0) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    constexpr int TR = tile_rows<T>(), AW = alive_words<T>(), W = TR / 32;  // words per bit-line
+    constexpr int NW = kDensifyThreads / 32, RW = TR / NW;
+    uint32_t* stage = reinterpret_cast<uint32_t*>(dsm);  // [kc][W]
+    __shared__ int64_t s_pos[TR], s_end[TR];
+    __shared__ uint32_t s_alive[AW];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < kc * W; i += blockDim.x) stage[i] = 0u;
+    const int n_spans = (n_in + span - 1) / span;
+    for (int bb = blockIdx.x; bb < n_tiles * n_spans; bb += gridDim.x) {
+        const int t = bb / n_spans;
+        const int kbeg = (bb % n_spans) * span, kend = min(n_in, kbeg + span);
+        if (tid < AW) s_alive[tid] = 0u;
+        __syncthreads();
+        for (int r = tid; r < TR; r += blockDim.x) {
+            const int row = rowid[(size_t)t * TR + r];
+            const int64_t p = row >= 0 ? csr_off[row] : 0, e = row >= 0 ? csr_off[row + 1] : 0;
+            if (e > p) {
+                atomicOr(&s_alive[r / 32], 1u << (r % 32));
+                atomicOr(&s_alive[AW - 1], 1u);
+            }
+            int64_t lo = p, hi = e;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (load_col(csr_cols, col_bytes, mid) < kbeg) lo = mid + 1;
+                else hi = mid;
+            }
+            s_pos[r] = lo;
+            s_end[r] = e;
+        }
+        __syncthreads();
+        int cb[RW];
+#pragma unroll
+        for (int i = 0; i < RW; ++i) {
+            const int r = warp + i * NW;
+            const int64_t q = s_pos[r] + lane;
+            cb[i] = q < s_end[r] ? load_col(csr_cols, col_bytes, q) : INT32_MAX;
+        }
+        char* s0 = reinterpret_cast<char*>(slab0 + (size_t)t * ld * TR);
+        uint2* gm = meta0 + (size_t)t * ld;
+        for (int k0 = kbeg; k0 < kend; k0 += kc) {
+            const int kn = min(kc, kend - k0);
+            bool mine = false;
+#pragma unroll
+            for (int i = 0; i < RW; ++i) mine |= cb[i] < k0 + kn;
+            if (!__syncthreads_or(mine)) continue;
+            for (bool refilled = true; refilled;) {
+                refilled = false;
+#pragma unroll
+                for (int i = 0; i < RW; ++i) {
+                    if (cb[i] < k0 + kn) {
+                        const int r = warp + i * NW;
+                        atomicOr(&stage[(cb[i] - k0) * W + r / 32], 1u << (r % 32));
+                        cb[i] = INT32_MAX;
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < RW; ++i) {
+                    const int r = warp + i * NW;
+                    if (__any_sync(0xffffffffu, cb[i] != INT32_MAX)) continue;
+                    const int64_t base = s_pos[r] + 32;
+                    if (base >= s_end[r]) continue;
+                    __syncwarp();
+                    if (lane == 0) s_pos[r] = base;
+                    __syncwarp();
+                    const int64_t q = base + lane;
+                    cb[i] = q < s_end[r] ? load_col(csr_cols, col_bytes, q) : INT32_MAX;
+                    refilled = true;
+                }
+            }
+            __syncthreads();
+            // one thread per line: append nonzero bit-lines to the heap
+            for (int k = tid; k < kn; k += blockDim.x) {
+                uint32_t wv[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+                uint32_t any = 0u;
+#pragma unroll
+                for (int q = 0; q < W; ++q) {
+                    wv[q] = stage[k * W + q];
+                    stage[k * W + q] = 0u;
+                    any |= wv[q];
+                }
+                if (any) {
+                    const unsigned base = atomicAdd(&heap0[t], 1u);
+                    uint4* dst = reinterpret_cast<uint4*>(s0 + (size_t)base * 32);
+                    dst[0] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                    dst[1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
+                    gm[k0 + k] = make_uint2(0xFFFFFFFFu, base);
+                }
+            }
+            __syncthreads();
+        }
+        __syncthreads();
+        if (tid < AW - 1 && s_alive[tid]) atomicOr(&alive0[(size_t)t * AW + tid], s_alive[tid]);
+        if (tid == AW - 1 && s_alive[tid] && atomicOr(&alive0[(size_t)t * AW + tid], 1u) == 0u)
+            atomicAdd(tile_count0, 1);
+    }
+}
+
 // ------------------------------------------------------------ one item
 // Output columns [j0, j1) of tile t for layer l: warp per column.
 // The warp walks its columns' 32-slot batches with a three-stage prefetch
@@ -396,7 +509,7 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_kernel(const int64_t*
 // multiple of GB with zero-line, zero-weight entries), which is then
 // gathered GB lines at a time, double-buffered when DBUF.  Each lane chains
 // its RPL rows separately; one 256-bit load per lane per line.
-template <typename T, int GB, bool DBUF, bool PRED>
+template <typename T, int GB, bool DBUF, bool PRED, bool BIN>
 __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<T>& L, int l, int t,
                                            int j0, int j1, SlotEntry<T>* wlist) {
     using A = Arith<T>;
@@ -474,40 +587,68 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
             if (at < npad) wlist[at] = e;
         }
         __syncwarp();
-        auto issue = [&](T (&y)[GB][RPL], int i0) {
+        if (BIN) {
+            // binary input lines: 32 bytes per line, lane l's RPL rows are
+            // bits l*RPL.. of it; a set bit adds w to the row's chain (the
+            // same rounding as y*w + acc with y = 1), a clear bit adds nothing
+            constexpr unsigned kMaskBits = (1u << RPL) - 1u;
+            const int bpos = lane * RPL;
+            for (int i0 = 0; i0 < npad; i0 += GB) {
+                unsigned by[GB];
 #pragma unroll
-            for (int u = 0; u < GB; ++u) {
-                const SlotEntry<T> e = wlist[i0 + u];
-                if (PRED)  // dead lanes: no request, zeros (adding +-0 never changes a chain)
-                    ld32_pred(y[u], in + (size_t)(e.base + __popc(e.mask & below)) * 32, (e.mask & lbit) != 0u);
-                else       // dead lanes read the shared zero sector (an L1 hit)
-                    ld32(y[u], (e.mask & lbit) ? in + (size_t)(e.base + __popc(e.mask & below)) * 32 : zsec);
-            }
-        };
-        auto consume = [&](const T (&y)[GB][RPL], int i0) {
+                for (int u = 0; u < GB; ++u) {
+                    const SlotEntry<T> e = wlist[i0 + u];
+                    by[u] = e.mask ? (unsigned)__ldg(reinterpret_cast<const unsigned char*>(in) +
+                                                     (size_t)e.base * 32 + (bpos >> 3))
+                                   : 0u;
+                }
 #pragma unroll
-            for (int u = 0; u < GB; ++u) {
-                const T w = wlist[i0 + u].w;
+                for (int u = 0; u < GB; ++u) {
+                    const T w = wlist[i0 + u].w;
+                    const unsigned bits = (by[u] >> (bpos & 7)) & kMaskBits;
 #pragma unroll
-                for (int c = 0; c < RPL; ++c) acc[c] = A::muladd(y[u][c], w, acc[c]);
-            }
-        };
-        if (DBUF) {
-            // the next sub-batch's loads are in flight while this one is consumed
-            T ya[GB][RPL], yb[GB][RPL];
-            if (npad) issue(ya, 0);
-            for (int i0 = 0; i0 < npad; i0 += 2 * GB) {
-                if (i0 + GB < npad) issue(yb, i0 + GB);
-                consume(ya, i0);
-                if (i0 + GB >= npad) break;
-                if (i0 + 2 * GB < npad) issue(ya, i0 + 2 * GB);
-                consume(yb, i0 + GB);
+                    for (int c = 0; c < RPL; ++c) {
+                        const T s1 = A::add(acc[c], w);
+                        acc[c] = ((bits >> c) & 1u) ? s1 : acc[c];
+                    }
+                }
             }
         } else {
-            for (int i0 = 0; i0 < npad; i0 += GB) {
-                T y[GB][RPL];
-                issue(y, i0);
-                consume(y, i0);
+            auto issue = [&](T (&y)[GB][RPL], int i0) {
+#pragma unroll
+                for (int u = 0; u < GB; ++u) {
+                    const SlotEntry<T> e = wlist[i0 + u];
+                    if (PRED)  // dead lanes: no request, zeros (adding +-0 never changes a chain)
+                        ld32_pred(y[u], in + (size_t)(e.base + __popc(e.mask & below)) * 32, (e.mask & lbit) != 0u);
+                    else       // dead lanes read the shared zero sector (an L1 hit)
+                        ld32(y[u], (e.mask & lbit) ? in + (size_t)(e.base + __popc(e.mask & below)) * 32 : zsec);
+                }
+            };
+            auto consume = [&](const T (&y)[GB][RPL], int i0) {
+#pragma unroll
+                for (int u = 0; u < GB; ++u) {
+                    const T w = wlist[i0 + u].w;
+#pragma unroll
+                    for (int c = 0; c < RPL; ++c) acc[c] = A::muladd(y[u][c], w, acc[c]);
+                }
+            };
+            if (DBUF) {
+                // the next sub-batch's loads are in flight while this one is consumed
+                T ya[GB][RPL], yb[GB][RPL];
+                if (npad) issue(ya, 0);
+                for (int i0 = 0; i0 < npad; i0 += 2 * GB) {
+                    if (i0 + GB < npad) issue(yb, i0 + GB);
+                    consume(ya, i0);
+                    if (i0 + GB >= npad) break;
+                    if (i0 + 2 * GB < npad) issue(ya, i0 + 2 * GB);
+                    consume(yb, i0 + GB);
+                }
+            } else {
+                for (int i0 = 0; i0 < npad; i0 += GB) {
+                    T y[GB][RPL];
+                    issue(y, i0);
+                    consume(y, i0);
+                }
             }
         }
         __syncwarp();
@@ -601,7 +742,10 @@ __global__ void __launch_bounds__(kThreads, (DBUF ? 2 * GB : GB) * 8 <= 32 ? 3 :
             const int t = tiles[it / nblk];
             const int bb = (int)(it % nblk);
             const int j0 = bb * a.jb, j1 = min(a.n_out, j0 + a.jb);
-            layer_item<T, GB, DBUF, PRED>(a, L, l, t, j0, j1, s_list[warp]);
+            if (l == 0 && a.bin_in)
+                layer_item<T, 8, false, false, true>(a, L, l, t, j0, j1, s_list[warp]);
+            else
+                layer_item<T, GB, DBUF, PRED, false>(a, L, l, t, j0, j1, s_list[warp]);
         }
         grid_barrier(a.bar, nb);
         if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[l + 1] = globaltimer();

@@ -337,3 +337,37 @@ def test_c5_sweep_cells(batch, p):
     assert O.CSR(rows, w.n, *head.y).identical(want)
     assert np.array_equal(full.categories[full.categories <= rows], O.categorize(want))
     net.close()
+
+
+@pytest.mark.parametrize("dtype,prec", [("f64", 64), ("f32", 32)])
+def test_real_valued_inputs_use_the_float_tiles(dtype, prec):
+    """Y0 with arbitrary values (not the binary images): values are uploaded
+    and expanded into float tiles; results must match the oracle bit for bit."""
+    w, y0, layers = permunion_case(1024, 6, 300, 0.125)
+    rng = np.random.default_rng(11)
+    vals = rng.uniform(0.05, 2.0, size=y0.vals.size)
+    y0 = O.CSR(y0.n_rows, y0.n_cols, y0.off, y0.cols, vals)
+    net = E.DeviceNetwork(w.n, 0, dtype)
+    for l in range(w.layers):
+        net.add_layer_csr(sm(layers[l]), w.bias)
+    batch = net.upload_csr(y0.n_rows, y0.off, y0.cols, y0.vals)
+    assert batch.h2d_bytes >= y0.vals.size * (8 if dtype == "f64" else 4)
+    res = net.run(batch, w.ymax, want_y=True)
+    want = O.infer(layers, [w.bias] * w.layers, y0, precision=prec, threads=4)
+    assert O.CSR(y0.n_rows, w.n, *res.y).identical(want)
+
+
+def test_binary_inputs_bit_tiles_and_float_tiles_agree(env):
+    """The binary-image fast path (bit-line tiles for layer 1) and the
+    general float tiles give identical bits."""
+    t_cases = goldens.general()[:16]
+    outs = []
+    for flag in ("1", "0"):
+        env["SDNN_BIN"] = flag
+        res = []
+        for t in t_cases:
+            model = model_of(t["layers"], t["bias"], t["n"])
+            res.append(as_csr(E.infer(model, FeatureBatch(sm(t["y0"])))))
+        outs.append(res)
+    for a, b, t in zip(outs[0], outs[1], t_cases):
+        assert a.identical(b) and a.identical(t["y"])
