@@ -734,6 +734,12 @@ int make_net(int device, int dtype, int64_t n, sdnn_net** out) {
     net->elem = dtype == SDNN_F64 ? 8 : 4;
     CK(cudaDeviceGetAttribute(&net->sm_count, cudaDevAttrMultiProcessorCount, device));
     CK(cudaStreamCreateWithFlags(&net->stream, cudaStreamNonBlocking));
+    {  // keep freed upload buffers in the stream-ordered pool between calls
+        cudaMemPool_t pool;
+        CK(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t keep = UINT64_MAX;
+        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     CK(cudaEventCreate(&net->ev0));
     CK(cudaEventCreate(&net->ev1));
     *out = net;
