@@ -518,7 +518,18 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
         CK(cudaGetLastError());
         res->launches += 1;
     }
-    CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, smem, net->stream));
+    if (a.bin_in) {  // layer 1 over bit-line tiles: its own launch
+        const void* bfn = (const void*)bin_layer_kernel<T>;
+        CK(cudaFuncSetAttribute(bfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int bocc = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bocc, bfn, kThreads, smem));
+        bin_layer_kernel<T><<<net->sm_count * std::max(bocc, 1), kThreads, smem, net->stream>>>(a);
+        CK(cudaGetLastError());
+        res->launches += 1;
+        a.first_l = 1;
+    }
+    if (a.first_l < a.L)
+        CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, smem, net->stream));
     CK(cudaEventRecord(net->ev1, net->stream));
     res->launches += 1;
     live_rows_kernel<<<(unsigned)(nl + 1), 256, 0, net->stream>>>(net->alive, (int)tiles1, AW, live);

@@ -194,6 +194,7 @@ struct NetArgs {
     unsigned long long* stamps;  // [L + 1] globaltimer after each layer, or null
     int jb;               // outputs per work item
     int bin_in;           // layer-0 input is bit-lines (binary Y0)
+    int first_l;          // first layer net_kernel runs (1 after bin_layer_kernel)
 };
 
 constexpr int kThreads = 256;
@@ -607,10 +608,8 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
                     const T w = wlist[i0 + u].w;
                     const unsigned bits = (by[u] >> (bpos & 7)) & kMaskBits;
 #pragma unroll
-                    for (int c = 0; c < RPL; ++c) {
-                        const T s1 = A::add(acc[c], w);
-                        acc[c] = ((bits >> c) & 1u) ? s1 : acc[c];
-                    }
+                    for (int c = 0; c < RPL; ++c)
+                        if ((bits >> c) & 1u) acc[c] = A::add(acc[c], w);  // R2P + predicated adds
                 }
             }
         } else {
@@ -682,71 +681,95 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
 }
 
 // GB = lines gathered per sub-batch per warp.
+// Shared state of one CTA's walk over a layer.
+template <typename T>
+struct LayerShared {
+    SlotEntry<T> list[kWarps][32];
+    int count;
+    int scan[kWarps + 1];
+    long long item;
+};
+
+// One layer for this CTA: build the ascending live-tile list from the
+// layer's alive flags, then take (tile, output block) items in order from the
+// layer's counter until none are left.
+template <typename T, int GB, bool DBUF, bool PRED, bool BIN>
+__device__ __forceinline__ void layer_pass(const NetArgs<T>& a, int l, int32_t* tiles, LayerShared<T>& sh) {
+    constexpr int AW = alive_words<T>();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t* alive_in = a.alive + (size_t)l * a.n_tiles * AW;
+    if (tid == 0) sh.count = 0;
+    __syncthreads();
+    for (int base = 0; base < a.n_tiles; base += kThreads) {
+        const int t = base + tid;
+        const bool live = t < a.n_tiles && __ldcg(&alive_in[(size_t)t * AW + AW - 1]) != 0u;
+        const unsigned b = __ballot_sync(0xffffffffu, live);
+        if (lane == 0) sh.scan[warp] = __popc(b);
+        __syncthreads();
+        if (tid == 0) {
+            int acc = sh.count;
+            for (int w = 0; w < kWarps; ++w) {
+                const int c = sh.scan[w];
+                sh.scan[w] = acc;
+                acc += c;
+            }
+            sh.scan[kWarps] = acc;
+        }
+        __syncthreads();
+        if (live) tiles[sh.scan[warp] + __popc(b & ((1u << lane) - 1u))] = t;
+        __syncthreads();
+        if (tid == 0) sh.count = sh.scan[kWarps];
+        __syncthreads();
+    }
+    const int count = sh.count;
+    const LayerDesc<T> L = a.layers[l];
+    const int nblk = (a.n_out + a.jb - 1) / a.jb;
+    const long long items = (long long)count * nblk;
+    // items are handed out in order from a counter, so all CTAs work on a
+    // narrow window of tiles and the tiles' input lines stay in L2 across
+    // the 32 columns that gather each of them
+    for (;;) {
+        if (tid == 0) sh.item = (long long)atomicAdd(&a.work[l], 1u);
+        __syncthreads();
+        const long long it = sh.item;
+        __syncthreads();
+        if (it >= items) break;
+        const int t = tiles[it / nblk];
+        const int bb = (int)(it % nblk);
+        const int j0 = bb * a.jb, j1 = min(a.n_out, j0 + a.jb);
+        layer_item<T, GB, DBUF, PRED, BIN>(a, L, l, t, j0, j1, sh.list[warp]);
+    }
+}
+
+// Layer 1 over binary bit-line tiles, as its own launch so its small
+// register footprint buys more resident warps than the float path's.
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 4) bin_layer_kernel(NetArgs<T> a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ LayerShared<T> sh;
+    if (a.stamps && blockIdx.x == 0 && threadIdx.x == 0) a.stamps[0] = globaltimer();
+    if (__ldcg(&a.tile_count[0]) == 0) return;
+    layer_pass<T, 8, false, false, true>(a, 0, reinterpret_cast<int32_t*>(smem), sh);
+}
+
+// All remaining layers (from a.first_l) in one cooperative launch with a
+// grid barrier between live layers.
 template <typename T, int GB, bool DBUF, bool PRED>
 __global__ void __launch_bounds__(kThreads, (DBUF ? 2 * GB : GB) * 8 <= 32 ? 3 : 2)  // y registers
     net_kernel(NetArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem[];
     int32_t* tiles = reinterpret_cast<int32_t*>(smem);
-    __shared__ SlotEntry<T> s_list[kWarps][32];
-    __shared__ int s_count;
-    __shared__ int s_scan[kWarps + 1];
-    __shared__ long long s_item;
-    constexpr int AW = alive_words<T>();
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ LayerShared<T> sh;
+    const int tid = threadIdx.x;
     const unsigned nb = gridDim.x;
-    if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[0] = globaltimer();
+    if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[a.first_l] = globaltimer();
 
     bool all_dead = false;
-    for (int l = 0; l < a.L; ++l) {
+    for (int l = a.first_l; l < a.L; ++l) {
         // zero rows stay zero: once no tile is live every later layer is empty
         if (!all_dead && __ldcg(&a.tile_count[l]) == 0) all_dead = true;
         if (all_dead) continue;
-        const uint32_t* alive_in = a.alive + (size_t)l * a.n_tiles * AW;
-        // ascending live-tile list (block-wide ordered compaction)
-        if (tid == 0) s_count = 0;
-        __syncthreads();
-        for (int base = 0; base < a.n_tiles; base += kThreads) {
-            const int t = base + tid;
-            const bool live = t < a.n_tiles && __ldcg(&alive_in[(size_t)t * AW + AW - 1]) != 0u;
-            const unsigned b = __ballot_sync(0xffffffffu, live);
-            if (lane == 0) s_scan[warp] = __popc(b);
-            __syncthreads();
-            if (tid == 0) {
-                int acc = s_count;
-                for (int w = 0; w < kWarps; ++w) {
-                    const int c = s_scan[w];
-                    s_scan[w] = acc;
-                    acc += c;
-                }
-                s_scan[kWarps] = acc;
-            }
-            __syncthreads();
-            if (live) tiles[s_scan[warp] + __popc(b & ((1u << lane) - 1u))] = t;
-            __syncthreads();
-            if (tid == 0) s_count = s_scan[kWarps];
-            __syncthreads();
-        }
-        const int count = s_count;
-        const LayerDesc<T> L = a.layers[l];
-        const int nblk = (a.n_out + a.jb - 1) / a.jb;
-        const long long items = (long long)count * nblk;
-        // items are handed out in order from a counter, so all CTAs work on
-        // a narrow window of tiles and the tiles' input lines stay in L2
-        // across the 32 columns that gather each of them
-        for (;;) {
-            if (tid == 0) s_item = (long long)atomicAdd(&a.work[l], 1u);
-            __syncthreads();
-            const long long it = s_item;
-            __syncthreads();
-            if (it >= items) break;
-            const int t = tiles[it / nblk];
-            const int bb = (int)(it % nblk);
-            const int j0 = bb * a.jb, j1 = min(a.n_out, j0 + a.jb);
-            if (l == 0 && a.bin_in)
-                layer_item<T, 8, false, false, true>(a, L, l, t, j0, j1, s_list[warp]);
-            else
-                layer_item<T, GB, DBUF, PRED, false>(a, L, l, t, j0, j1, s_list[warp]);
-        }
+        layer_pass<T, GB, DBUF, PRED, false>(a, l, tiles, sh);
         grid_barrier(a.bar, nb);
         if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[l + 1] = globaltimer();
     }
