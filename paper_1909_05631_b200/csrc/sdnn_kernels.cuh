@@ -594,8 +594,7 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
             // same rounding as y*w + acc with y = 1), a clear bit adds nothing
             constexpr unsigned kMaskBits = (1u << RPL) - 1u;
             const int bpos = lane * RPL;
-            for (int i0 = 0; i0 < npad; i0 += GB) {
-                unsigned by[GB];
+            auto issue_b = [&](unsigned (&by)[GB], int i0) {
 #pragma unroll
                 for (int u = 0; u < GB; ++u) {
                     const SlotEntry<T> e = wlist[i0 + u];
@@ -603,6 +602,8 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
                                                      (size_t)e.base * 32 + (bpos >> 3))
                                    : 0u;
                 }
+            };
+            auto consume_b = [&](const unsigned (&by)[GB], int i0) {
 #pragma unroll
                 for (int u = 0; u < GB; ++u) {
                     const T w = wlist[i0 + u].w;
@@ -611,6 +612,16 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
                     for (int c = 0; c < RPL; ++c)
                         if ((bits >> c) & 1u) acc[c] = A::add(acc[c], w);  // R2P + predicated adds
                 }
+            };
+            // two sub-batches of byte loads in flight
+            unsigned ba[GB], bb[GB];
+            if (npad) issue_b(ba, 0);
+            for (int i0 = 0; i0 < npad; i0 += 2 * GB) {
+                if (i0 + GB < npad) issue_b(bb, i0 + GB);
+                consume_b(ba, i0);
+                if (i0 + GB >= npad) break;
+                if (i0 + 2 * GB < npad) issue_b(ba, i0 + 2 * GB);
+                consume_b(bb, i0 + GB);
             }
         } else {
             auto issue = [&](T (&y)[GB][RPL], int i0) {
