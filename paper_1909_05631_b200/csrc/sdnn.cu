@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <chrono>
 #include <cstdarg>
 #include <cstdio>
@@ -139,6 +140,7 @@ struct sdnn_batch {
     int64_t* off = nullptr;
     void* cols = nullptr;
     void* vals = nullptr;     // null: every stored value is 1.0
+    bool finite = true;       // every stored value is finite (as T)
 };
 
 struct sdnn_result {
@@ -468,18 +470,11 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     const size_t dsmem = (size_t)kc * kLineBytes;
     const void* dfn = (const void*)densify_kernel<T>;
     CK(cudaFuncSetAttribute(dfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
-    // gather pipeline: 1 = register double-buffered 4-line sub-batches
-    // (default), 2 = (2 lines, double-buffered), 3 = (4 lines, single).
-    // (A per-warp TMA bulk-copy ring was measured 1.5x slower: one bulk
-    // copy per <= 1 KB line is below the TMA unit's efficient size.)
-    // dead sectors: 1 = predicated off, no request (default; the L1 data path
-    // is the limit for sparse lines), 0 = read the shared zero sector
-    const int kvar = env_int("SDNN_KVAR", 1);
-    const int pred_loads = env_int("SDNN_PRED", 1);
-    const void* fn = kvar == 2   ? (const void*)net_kernel<T, 2, true, false>
-                     : kvar == 3 ? (const void*)net_kernel<T, 4, false, false>
-                     : pred_loads ? (const void*)net_kernel<T, 4, true, true>
-                                  : (const void*)net_kernel<T, 4, true, false>;
+    // Dead-sector handling in the gather: without zero-fill a dead lane keeps
+    // its previous (finite) registers and adds them with weight 0, which is
+    // exact only when every value the kernel can read is finite.
+    const bool zfill = !batch->finite || !std::isfinite((T)ymax) || env_int("SDNN_ZFILL", 0) != 0;
+    const void* fn = zfill ? (const void*)net_kernel<T, 4, true> : (const void*)net_kernel<T, 4, false>;
     const size_t smem = (size_t)tiles1 * 4;
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
@@ -673,8 +668,13 @@ int upload_csr(sdnn_net* net, int64_t n_rows, const int64_t* off, const int64_t*
             const int64_t c1 = std::min(nnz, c0 + chunk);
             CK(cudaEventSynchronize(net->stage_ev[buf]));
             T* dst = reinterpret_cast<T*>(stage[buf]);
-#pragma omp parallel for schedule(static)
-            for (int64_t p = c0; p < c1; ++p) dst[p - c0] = (T)vals[p];
+            int chunk_fin = 1;
+#pragma omp parallel for reduction(& : chunk_fin) schedule(static)
+            for (int64_t p = c0; p < c1; ++p) {
+                dst[p - c0] = (T)vals[p];
+                chunk_fin &= std::isfinite(dst[p - c0]) ? 1 : 0;
+            }
+            b->finite = b->finite && chunk_fin;
             CK(cudaMemcpyAsync(reinterpret_cast<T*>(b->vals) + c0, dst, (c1 - c0) * sizeof(T), cudaMemcpyHostToDevice,
                                net->stream));
             CK(cudaEventRecord(net->stage_ev[buf], net->stream));

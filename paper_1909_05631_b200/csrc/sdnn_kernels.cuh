@@ -64,11 +64,9 @@ template <> struct Arith<double> {
 // unstored entry and receives no bias (entry-masked bias).
 template <typename T>
 __device__ __forceinline__ T bias_relu_clamp(T acc, T bias, T ymax) {
-    if (acc != T(0)) {
-        T v = Arith<T>::add(acc, bias);
-        if (v > T(0)) return v > ymax ? ymax : v;
-    }
-    return T(0);
+    const T v = Arith<T>::add(acc, bias);
+    const T c = v > ymax ? ymax : v;
+    return (acc != T(0) && v > T(0)) ? c : T(0);  // selects, no branches
 }
 
 // engine.py:129-133 on one STORED entry (CSR path: stored means present).
@@ -90,14 +88,6 @@ template <typename T>
 __host__ __device__ constexpr int alive_words() { return tile_rows<T>() / 32 + 1; }
 
 // One lane's 32-byte sector <-> its RPL values (256-bit accesses).
-__device__ __forceinline__ void ld32(float (&d)[8], const char* p) {
-    asm("ld.global.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-        : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3]), "=f"(d[4]), "=f"(d[5]), "=f"(d[6]), "=f"(d[7])
-        : "l"(p));
-}
-__device__ __forceinline__ void ld32(double (&d)[4], const char* p) {
-    asm("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(d[0]), "=d"(d[1]), "=d"(d[2]), "=d"(d[3]) : "l"(p));
-}
 // Predicated 256-bit gather: zeros without any memory request when the
 // lane's sector is not live.
 __device__ __forceinline__ void ld32_pred(float (&d)[8], const char* p, bool live) {
@@ -113,6 +103,21 @@ __device__ __forceinline__ void ld32_pred(double (&d)[4], const char* p, bool li
         "mov.b64 %0, 0;\n\tmov.b64 %1, 0;\n\tmov.b64 %2, 0;\n\tmov.b64 %3, 0;\n\t"
         "@q ld.global.v4.f64 {%0, %1, %2, %3}, [%4];\n\t}"
         : "=d"(d[0]), "=d"(d[1]), "=d"(d[2]), "=d"(d[3])
+        : "l"(p), "r"((unsigned)live));
+}
+
+// Predicated 256-bit gather that leaves the registers as they were when the
+// lane's sector is not live (the caller zeroes the lane's weight instead).
+__device__ __forceinline__ void ld32_keep(float (&d)[8], const char* p, bool live) {
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %9, 0;\n\t"
+        "@q ld.global.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n\t}"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3]), "+f"(d[4]), "+f"(d[5]), "+f"(d[6]), "+f"(d[7])
+        : "l"(p), "r"((unsigned)live));
+}
+__device__ __forceinline__ void ld32_keep(double (&d)[4], const char* p, bool live) {
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t"
+        "@q ld.global.v4.f64 {%0, %1, %2, %3}, [%4];\n\t}"
+        : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
         : "l"(p), "r"((unsigned)live));
 }
 
@@ -158,10 +163,10 @@ __device__ __forceinline__ double ld_w(const double* p, uint64_t pol) {
     return v;
 }
 
-// One live slot of a warp's compacted slot list (16 bytes).
+// One live slot of a warp's compacted slot list (16 bytes for float).
 template <typename T>
 struct __align__(16) SlotEntry {
-    unsigned base;  // heap index of the line's first kept sector
+    const char* p;  // the line's first kept sector in the input heap
     unsigned mask;  // lanes whose sector of that line is kept (nonzero)
     T w;            // weight
 };
@@ -504,13 +509,18 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_bin_kernel(const int6
 // Output columns [j0, j1) of tile t for layer l: warp per column.
 // The warp walks its columns' 32-slot batches with a three-stage prefetch
 // (slot indices + weights two batches ahead, the lines' sector masks one
-// batch ahead).  In a batch, lane s holds slot s (input line offset, sector
-// mask, weight); slots whose line is entirely zero are dropped and the rest
-// are compacted, in slot order, into the warp's smem list (padded to a
-// multiple of GB with zero-line, zero-weight entries), which is then
-// gathered GB lines at a time, double-buffered when DBUF.  Each lane chains
-// its RPL rows separately; one 256-bit load per lane per line.
-template <typename T, int GB, bool DBUF, bool PRED, bool BIN>
+// batch ahead).  In a batch, lane s holds slot s (input line, sector mask,
+// weight); slots whose line is entirely zero are dropped and the rest are
+// compacted, in slot order, into the warp's smem list (padded to a multiple
+// of GB with entries no lane gathers), which is then gathered GB lines at a
+// time, double-buffered in registers.  Each lane chains its RPL rows
+// separately; one 256-bit load per lane per line, none for a dead sector.
+//
+// Dead lanes: with ZFILL the predicated-off load zero-fills its registers;
+// without it the registers keep the lane's previous (finite) values and the
+// lane's weight is 0 instead, y*0 + acc == acc.  The host picks ZFILL unless
+// every value the kernel can read is finite (Y0 finite and ymax finite).
+template <typename T, int GB, bool BIN, bool ZFILL>
 __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<T>& L, int l, int t,
                                            int j0, int j1, SlotEntry<T>* wlist) {
     using A = Arith<T>;
@@ -538,49 +548,66 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
             if (lane == 0) ometa[j] = make_uint2(0u, 0u);
         return;
     }
-    auto slot_ptr = [&](int b) {
-        const int j = jw + (b / nb) * kWarps;
-        return (size_t)j * L.wp + (size_t)(b % nb) * 32 + lane;
+    // slot cursor of the next batch to prefetch: columns jw, jw + kWarps, ...
+    // each nb batches of 32 slots (no divisions in the loop)
+    size_t po = (size_t)jw * L.wp + lane;
+    int pb = 0;
+    const size_t col_skip = (size_t)(kWarps - 1) * L.wp;
+    auto advance = [&]() {
+        po += 32;
+        if (++pb == nb) {
+            pb = 0;
+            po += col_skip;
+        }
     };
     // pipeline registers: (k1, w1) for batch b+1, (k2, w2) for batch b+2
     const uint64_t wpol = policy_evict_last();
-    int k0 = ld_w(L.idx + slot_ptr(0), wpol);
-    T w0 = ld_w(L.val + slot_ptr(0), wpol);
+    int k0 = ld_w(L.idx + po, wpol);
+    T w0 = ld_w(L.val + po, wpol);
+    advance();
     int k1 = -1, k2 = -1;
     T w1 = T(0), w2 = T(0);
     if (total > 1) {
-        k1 = ld_w(L.idx + slot_ptr(1), wpol);
-        w1 = ld_w(L.val + slot_ptr(1), wpol);
+        k1 = ld_w(L.idx + po, wpol);
+        w1 = ld_w(L.val + po, wpol);
+        advance();
     }
     uint2 m0 = k0 >= 0 ? imeta[k0] : make_uint2(0u, 0u);
     T acc[RPL];
     unsigned alive_bits = 0u;
 #pragma unroll
     for (int c = 0; c < RPL; ++c) acc[c] = T(0);
+    // gather registers (loop-carried: without ZFILL a dead lane keeps them)
+    T ya[GB][RPL], yb[GB][RPL];
+    T wa[GB], wb[GB];
+#pragma unroll
+    for (int u = 0; u < GB; ++u) {
+#pragma unroll
+        for (int c = 0; c < RPL; ++c) ya[u][c] = yb[u][c] = T(0);
+    }
+    int cj = jw, cb = 0;  // current column and batch within it
     for (int b = 0; b < total; ++b) {
         // issue the next loads before working on batch b
         if (b + 2 < total) {
-            k2 = ld_w(L.idx + slot_ptr(b + 2), wpol);
-            w2 = ld_w(L.val + slot_ptr(b + 2), wpol);
+            k2 = ld_w(L.idx + po, wpol);
+            w2 = ld_w(L.val + po, wpol);
+            advance();
         }
         const uint2 m1 = (b + 1 < total && k1 >= 0) ? imeta[k1] : make_uint2(0u, 0u);
 
         const unsigned live = __ballot_sync(0xffffffffu, m0.x != 0u);
         const int n = __popc(live);
-        // the list is padded up to a multiple of GB with entries that read
-        // the zero line with weight 0 (adds +0, never changes a chain), so
-        // the gather loops below carry no per-slot guards
         const int npad = (n + GB - 1) / GB * GB;
         {
             SlotEntry<T> e;
             int at;
             if (m0.x) {
-                e.base = m0.y;
+                e.p = in + (size_t)m0.y * 32;
                 e.mask = m0.x;
                 e.w = w0;
                 at = __popc(live & below);
-            } else {  // padding: no lane live -> every lane reads the zero sector
-                e.base = 0u;
+            } else {  // padding: no lane gathers it (bit-lines: the zero line)
+                e.p = zsec;
                 e.mask = 0u;
                 e.w = T(0);
                 at = n + __popc(~live & below);
@@ -589,31 +616,27 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
         }
         __syncwarp();
         if (BIN) {
-            // binary input lines: 32 bytes per line, lane l's RPL rows are
-            // bits l*RPL.. of it; a set bit adds w to the row's chain (the
-            // same rounding as y*w + acc with y = 1), a clear bit adds nothing
+            // a set bit adds w to the row's chain (the same rounding as
+            // y*w + acc with y = 1), a clear bit adds nothing
+            // binary input lines: TR bits per line, lane l's RPL rows are
+            // bits l*RPL .. l*RPL+RPL-1 (float: byte l; double: half of byte l/2)
             constexpr unsigned kMaskBits = (1u << RPL) - 1u;
             const int bpos = lane * RPL;
             auto issue_b = [&](unsigned (&by)[GB], int i0) {
 #pragma unroll
-                for (int u = 0; u < GB; ++u) {
-                    const SlotEntry<T> e = wlist[i0 + u];
-                    by[u] = e.mask ? (unsigned)__ldg(reinterpret_cast<const unsigned char*>(in) +
-                                                     (size_t)e.base * 32 + (bpos >> 3))
-                                   : 0u;
-                }
+                for (int u = 0; u < GB; ++u)
+                    by[u] = ((unsigned)__ldg(reinterpret_cast<const unsigned char*>(wlist[i0 + u].p) + (bpos >> 3)) >>
+                             (bpos & 7)) & kMaskBits;
             };
             auto consume_b = [&](const unsigned (&by)[GB], int i0) {
 #pragma unroll
                 for (int u = 0; u < GB; ++u) {
                     const T w = wlist[i0 + u].w;
-                    const unsigned bits = (by[u] >> (bpos & 7)) & kMaskBits;
 #pragma unroll
                     for (int c = 0; c < RPL; ++c)
-                        if ((bits >> c) & 1u) acc[c] = A::add(acc[c], w);  // R2P + predicated adds
+                        if ((by[u] >> c) & 1u) acc[c] = A::add(acc[c], w);  // R2P + predicated adds
                 }
             };
-            // two sub-batches of byte loads in flight
             unsigned ba[GB], bb[GB];
             if (npad) issue_b(ba, 0);
             for (int i0 = 0; i0 < npad; i0 += 2 * GB) {
@@ -624,46 +647,41 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
                 consume_b(bb, i0 + GB);
             }
         } else {
-            auto issue = [&](T (&y)[GB][RPL], int i0) {
+            auto issue = [&](T (&y)[GB][RPL], T (&wv)[GB], int i0) {
 #pragma unroll
                 for (int u = 0; u < GB; ++u) {
                     const SlotEntry<T> e = wlist[i0 + u];
-                    if (PRED)  // dead lanes: no request, zeros (adding +-0 never changes a chain)
-                        ld32_pred(y[u], in + (size_t)(e.base + __popc(e.mask & below)) * 32, (e.mask & lbit) != 0u);
-                    else       // dead lanes read the shared zero sector (an L1 hit)
-                        ld32(y[u], (e.mask & lbit) ? in + (size_t)(e.base + __popc(e.mask & below)) * 32 : zsec);
+                    const bool lv = (e.mask & lbit) != 0u;
+                    const char* p = e.p + (size_t)__popc(e.mask & below) * 32;
+                    if (ZFILL) {
+                        ld32_pred(y[u], p, lv);
+                        wv[u] = e.w;
+                    } else {
+                        ld32_keep(y[u], p, lv);
+                        wv[u] = lv ? e.w : T(0);
+                    }
                 }
             };
-            auto consume = [&](const T (&y)[GB][RPL], int i0) {
+            auto consume = [&](const T (&y)[GB][RPL], const T (&wv)[GB]) {
 #pragma unroll
                 for (int u = 0; u < GB; ++u) {
-                    const T w = wlist[i0 + u].w;
 #pragma unroll
-                    for (int c = 0; c < RPL; ++c) acc[c] = A::muladd(y[u][c], w, acc[c]);
+                    for (int c = 0; c < RPL; ++c) acc[c] = A::muladd(y[u][c], wv[u], acc[c]);
                 }
             };
-            if (DBUF) {
-                // the next sub-batch's loads are in flight while this one is consumed
-                T ya[GB][RPL], yb[GB][RPL];
-                if (npad) issue(ya, 0);
-                for (int i0 = 0; i0 < npad; i0 += 2 * GB) {
-                    if (i0 + GB < npad) issue(yb, i0 + GB);
-                    consume(ya, i0);
-                    if (i0 + GB >= npad) break;
-                    if (i0 + 2 * GB < npad) issue(ya, i0 + 2 * GB);
-                    consume(yb, i0 + GB);
-                }
-            } else {
-                for (int i0 = 0; i0 < npad; i0 += GB) {
-                    T y[GB][RPL];
-                    issue(y, i0);
-                    consume(y, i0);
-                }
+            // the next sub-batch's loads are in flight while this one is consumed
+            if (npad) issue(ya, wa, 0);
+            for (int i0 = 0; i0 < npad; i0 += 2 * GB) {
+                if (i0 + GB < npad) issue(yb, wb, i0 + GB);
+                consume(ya, wa);
+                if (i0 + GB >= npad) break;
+                if (i0 + 2 * GB < npad) issue(ya, wa, i0 + 2 * GB);
+                consume(yb, wb);
             }
         }
         __syncwarp();
-        if (b % nb == nb - 1) {  // column complete: epilogue
-            const int j = jw + (b / nb) * kWarps;
+        if (++cb == nb) {  // column complete: epilogue
+            cb = 0;
             T v[RPL];
             unsigned bits = 0u;
 #pragma unroll
@@ -677,8 +695,9 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
             if (lane == 0 && om) hb = atomicAdd(heap_out, (unsigned)__popc(om));
             hb = __shfl_sync(0xffffffffu, hb, 0);
             if (bits) st32(out + (size_t)(hb + __popc(om & below)) * 32, v);
-            if (lane == 0) ometa[j] = make_uint2(om, hb);
+            if (lane == 0) ometa[cj] = make_uint2(om, hb);
             alive_bits |= bits;
+            cj += kWarps;
         }
         k0 = k1;
         w0 = w1;
@@ -704,7 +723,7 @@ struct LayerShared {
 // One layer for this CTA: build the ascending live-tile list from the
 // layer's alive flags, then take (tile, output block) items in order from the
 // layer's counter until none are left.
-template <typename T, int GB, bool DBUF, bool PRED, bool BIN>
+template <typename T, int GB, bool BIN, bool ZFILL>
 __device__ __forceinline__ void layer_pass(const NetArgs<T>& a, int l, int32_t* tiles, LayerShared<T>& sh) {
     constexpr int AW = alive_words<T>();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -748,7 +767,7 @@ __device__ __forceinline__ void layer_pass(const NetArgs<T>& a, int l, int32_t* 
         const int t = tiles[it / nblk];
         const int bb = (int)(it % nblk);
         const int j0 = bb * a.jb, j1 = min(a.n_out, j0 + a.jb);
-        layer_item<T, GB, DBUF, PRED, BIN>(a, L, l, t, j0, j1, sh.list[warp]);
+        layer_item<T, GB, BIN, ZFILL>(a, L, l, t, j0, j1, sh.list[warp]);
     }
 }
 
@@ -760,13 +779,13 @@ __global__ void __launch_bounds__(kThreads, 4) bin_layer_kernel(NetArgs<T> a) {
     __shared__ LayerShared<T> sh;
     if (a.stamps && blockIdx.x == 0 && threadIdx.x == 0) a.stamps[0] = globaltimer();
     if (__ldcg(&a.tile_count[0]) == 0) return;
-    layer_pass<T, 8, false, false, true>(a, 0, reinterpret_cast<int32_t*>(smem), sh);
+    layer_pass<T, 8, true, false>(a, 0, reinterpret_cast<int32_t*>(smem), sh);
 }
 
 // All remaining layers (from a.first_l) in one cooperative launch with a
 // grid barrier between live layers.
-template <typename T, int GB, bool DBUF, bool PRED>
-__global__ void __launch_bounds__(kThreads, (DBUF ? 2 * GB : GB) * 8 <= 32 ? 3 : 2)  // y registers
+template <typename T, int GB, bool ZFILL>
+__global__ void __launch_bounds__(kThreads, 2 * GB * 8 <= 32 ? 3 : 2)  // y registers
     net_kernel(NetArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem[];
     int32_t* tiles = reinterpret_cast<int32_t*>(smem);
@@ -780,7 +799,7 @@ __global__ void __launch_bounds__(kThreads, (DBUF ? 2 * GB : GB) * 8 <= 32 ? 3 :
         // zero rows stay zero: once no tile is live every later layer is empty
         if (!all_dead && __ldcg(&a.tile_count[l]) == 0) all_dead = true;
         if (all_dead) continue;
-        layer_pass<T, GB, DBUF, PRED, false>(a, l, tiles, sh);
+        layer_pass<T, GB, false, ZFILL>(a, l, tiles, sh);
         grid_barrier(a.bar, nb);
         if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[l + 1] = globaltimer();
     }
