@@ -7,12 +7,14 @@ object is missing or no CUDA device is visible, calls raise loudly.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 from .errors import CapacityError, from_code
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libsdnn.so"
+# SDNN_LIB selects another build of the same sources (tuning variants)
+LIB_PATH = Path(os.environ["SDNN_LIB"]) if os.environ.get("SDNN_LIB") else PKG / "libsdnn.so"
 GEN_PATH = PKG / "libsdnn_gen.so"
 
 i64, i32, u64, dbl, cint = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64, ctypes.c_double, ctypes.c_int

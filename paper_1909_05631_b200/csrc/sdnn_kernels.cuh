@@ -60,6 +60,16 @@ template <> struct Arith<double> {
     }
 };
 
+// Two float chains stepped by one packed instruction (FFMA2, sm_100): each
+// half is an independent fused multiply-add with round-to-nearest, the same
+// bits as two __fmaf_rn; the weight is broadcast to both halves.
+__device__ __forceinline__ void ffma2(float& a0, float& a1, float y0, float y1, float w) {
+    asm("{.reg .b64 a, y, w;\n\tmov.b64 a, {%0, %1};\n\tmov.b64 y, {%2, %3};\n\tmov.b64 w, {%4, %4};\n\t"
+        "fma.rn.f32x2 a, y, w, a;\n\tmov.b64 {%0, %1}, a;\n\t}"
+        : "+f"(a0), "+f"(a1)
+        : "f"(y0), "f"(y1), "f"(w));
+}
+
 // engine.py:129-133 applied to one dense position; a zero position is an
 // unstored entry and receives no bias (entry-masked bias).
 template <typename T>
@@ -163,13 +173,24 @@ __device__ __forceinline__ double ld_w(const double* p, uint64_t pol) {
     return v;
 }
 
-// One live slot of a warp's compacted slot list (16 bytes for float).
+// One live slot of a warp's compacted slot list: 16 bytes, read with one
+// 128-bit shared load per slot.
 template <typename T>
 struct __align__(16) SlotEntry {
-    const char* p;  // the line's first kept sector in the input heap
+    unsigned base;  // heap index of the line's first kept sector
     unsigned mask;  // lanes whose sector of that line is kept (nonzero)
     T w;            // weight
 };
+template <typename T>
+__device__ __forceinline__ SlotEntry<T> load_entry(const SlotEntry<T>* e) {
+    const uint4 r = *reinterpret_cast<const uint4*>(e);
+    SlotEntry<T> o;
+    o.base = r.x;
+    o.mask = r.y;
+    if constexpr (sizeof(T) == 4) o.w = __uint_as_float(r.z);
+    else o.w = __hiloint2double((int)r.w, (int)r.z);
+    return o;
+}
 
 template <typename T>
 struct LayerDesc {
@@ -532,11 +553,13 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
     // force a local-memory copy of it
     const bool odd = l & 1;
     const char* in = reinterpret_cast<const char*>(odd ? a.slab[1] : a.slab[0]) + tile_lines * kLineBytes;
+    // one opaque 64-bit base: sector addresses are then a single wide
+    // multiply-add (the compiler would otherwise re-add a uniform part)
+    asm("mov.b64 %0, %0;" : "+l"(in));
     char* out = reinterpret_cast<char*>(odd ? a.slab[0] : a.slab[1]) + tile_lines * kLineBytes;
     const uint2* imeta = (odd ? a.meta[1] : a.meta[0]) + tile_lines;
     uint2* ometa = (odd ? a.meta[0] : a.meta[1]) + tile_lines;
     uint32_t* heap_out = a.heap + (size_t)(l + 1) * a.n_tiles + t;
-    const char* zsec = reinterpret_cast<const char*>(a.zero);
     const unsigned below = lbit - 1u;
     const int jw = j0 + warp;
     if (jw >= j1) return;
@@ -602,12 +625,12 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
             SlotEntry<T> e;
             int at;
             if (m0.x) {
-                e.p = in + (size_t)m0.y * 32;
+                e.base = m0.y;
                 e.mask = m0.x;
                 e.w = w0;
                 at = __popc(live & below);
-            } else {  // padding: no lane gathers it (bit-lines: the zero line)
-                e.p = zsec;
+            } else {  // padding: no lane gathers it
+                e.base = 0u;
                 e.mask = 0u;
                 e.w = T(0);
                 at = n + __popc(~live & below);
@@ -622,37 +645,40 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
             // bits l*RPL .. l*RPL+RPL-1 (float: byte l; double: half of byte l/2)
             constexpr unsigned kMaskBits = (1u << RPL) - 1u;
             const int bpos = lane * RPL;
-            auto issue_b = [&](unsigned (&by)[GB], int i0) {
-#pragma unroll
-                for (int u = 0; u < GB; ++u)
-                    by[u] = ((unsigned)__ldg(reinterpret_cast<const unsigned char*>(wlist[i0 + u].p) + (bpos >> 3)) >>
-                             (bpos & 7)) & kMaskBits;
-            };
-            auto consume_b = [&](const unsigned (&by)[GB], int i0) {
+            auto issue_b = [&](unsigned (&by)[GB], T (&wv)[GB], int i0) {
 #pragma unroll
                 for (int u = 0; u < GB; ++u) {
-                    const T w = wlist[i0 + u].w;
+                    const SlotEntry<T> e = load_entry(wlist + i0 + u);
+                    by[u] = e.mask ? ((unsigned)__ldg(reinterpret_cast<const unsigned char*>(in) +
+                                                      (size_t)e.base * 32 + (bpos >> 3)) >> (bpos & 7)) & kMaskBits
+                                   : 0u;
+                    wv[u] = e.w;
+                }
+            };
+            auto consume_b = [&](const unsigned (&by)[GB], const T (&wv)[GB]) {
+#pragma unroll
+                for (int u = 0; u < GB; ++u) {
 #pragma unroll
                     for (int c = 0; c < RPL; ++c)
-                        if ((by[u] >> c) & 1u) acc[c] = A::add(acc[c], w);  // R2P + predicated adds
+                        if ((by[u] >> c) & 1u) acc[c] = A::add(acc[c], wv[u]);  // R2P + predicated adds
                 }
             };
             unsigned ba[GB], bb[GB];
-            if (npad) issue_b(ba, 0);
+            if (npad) issue_b(ba, wa, 0);
             for (int i0 = 0; i0 < npad; i0 += 2 * GB) {
-                if (i0 + GB < npad) issue_b(bb, i0 + GB);
-                consume_b(ba, i0);
+                if (i0 + GB < npad) issue_b(bb, wb, i0 + GB);
+                consume_b(ba, wa);
                 if (i0 + GB >= npad) break;
-                if (i0 + 2 * GB < npad) issue_b(ba, i0 + 2 * GB);
-                consume_b(bb, i0 + GB);
+                if (i0 + 2 * GB < npad) issue_b(ba, wa, i0 + 2 * GB);
+                consume_b(bb, wb);
             }
         } else {
             auto issue = [&](T (&y)[GB][RPL], T (&wv)[GB], int i0) {
 #pragma unroll
                 for (int u = 0; u < GB; ++u) {
-                    const SlotEntry<T> e = wlist[i0 + u];
+                    const SlotEntry<T> e = load_entry(wlist + i0 + u);
                     const bool lv = (e.mask & lbit) != 0u;
-                    const char* p = e.p + (size_t)__popc(e.mask & below) * 32;
+                    const char* p = in + (size_t)(e.base + __popc(e.mask & below)) * 32;
                     if (ZFILL) {
                         ld32_pred(y[u], p, lv);
                         wv[u] = e.w;
@@ -665,8 +691,13 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
             auto consume = [&](const T (&y)[GB][RPL], const T (&wv)[GB]) {
 #pragma unroll
                 for (int u = 0; u < GB; ++u) {
+                    if constexpr (sizeof(T) == 4) {
 #pragma unroll
-                    for (int c = 0; c < RPL; ++c) acc[c] = A::muladd(y[u][c], wv[u], acc[c]);
+                        for (int c = 0; c < RPL; c += 2) ffma2(acc[c], acc[c + 1], y[u][c], y[u][c + 1], wv[u]);
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < RPL; ++c) acc[c] = A::muladd(y[u][c], wv[u], acc[c]);
+                    }
                 }
             };
             // the next sub-batch's loads are in flight while this one is consumed
@@ -771,15 +802,22 @@ __device__ __forceinline__ void layer_pass(const NetArgs<T>& a, int l, int32_t* 
     }
 }
 
+#ifndef SDNN_BIN_GB
+#define SDNN_BIN_GB 4
+#endif
+#ifndef SDNN_BIN_OCC
+#define SDNN_BIN_OCC 4
+#endif
+constexpr int kBinGB = SDNN_BIN_GB;  // bit-lines per sub-batch per warp
 // Layer 1 over binary bit-line tiles, as its own launch so its small
 // register footprint buys more resident warps than the float path's.
 template <typename T>
-__global__ void __launch_bounds__(kThreads, 4) bin_layer_kernel(NetArgs<T> a) {
+__global__ void __launch_bounds__(kThreads, SDNN_BIN_OCC) bin_layer_kernel(NetArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ LayerShared<T> sh;
     if (a.stamps && blockIdx.x == 0 && threadIdx.x == 0) a.stamps[0] = globaltimer();
     if (__ldcg(&a.tile_count[0]) == 0) return;
-    layer_pass<T, 8, true, false>(a, 0, reinterpret_cast<int32_t*>(smem), sh);
+    layer_pass<T, kBinGB, true, false>(a, 0, reinterpret_cast<int32_t*>(smem), sh);
 }
 
 // All remaining layers (from a.first_l) in one cooperative launch with a

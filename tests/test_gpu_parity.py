@@ -371,3 +371,33 @@ def test_binary_inputs_bit_tiles_and_float_tiles_agree(env):
         outs.append(res)
     for a, b, t in zip(outs[0], outs[1], t_cases):
         assert a.identical(b) and a.identical(t["y"])
+
+
+@pytest.mark.parametrize("dtype,prec", [("f64", 64), ("f32", 32)])
+def test_non_finite_inputs_take_the_zero_fill_gather(dtype, prec):
+    """Y0 holding inf (and, in float32, values that overflow to inf) must not
+    leak into rows whose sector is dead: the host switches the gather to the
+    zero-filling variant and the result equals the oracle bit for bit."""
+    w, y0, layers = permunion_case(1024, 4, 300, 0.125)
+    rng = np.random.default_rng(12)
+    vals = rng.uniform(0.05, 2.0, size=y0.vals.size)
+    hit = rng.choice(vals.size, size=40, replace=False)
+    vals[hit[:20]] = np.inf
+    vals[hit[20:]] = 1e300  # finite in float64, inf once rounded to float32
+    y0 = O.CSR(y0.n_rows, y0.n_cols, y0.off, y0.cols, vals)
+    net = E.DeviceNetwork(w.n, 0, dtype)
+    for l in range(w.layers):
+        net.add_layer_csr(sm(layers[l]), w.bias)
+    res = net.run(net.upload_csr(y0.n_rows, y0.off, y0.cols, y0.vals), w.ymax, want_y=True)
+    want = O.infer(layers, [w.bias] * w.layers, y0, precision=prec, threads=4)
+    assert O.CSR(y0.n_rows, w.n, *res.y).identical(want)
+
+
+def test_zero_fill_and_keep_gathers_agree(env):
+    """Both dead-lane treatments of the gather (zero-filled registers, or kept
+    registers with weight 0) give the reference's bits."""
+    for flag in ("1", "0"):
+        env["SDNN_ZFILL"] = flag
+        for t in goldens.general()[:16]:
+            model = model_of(t["layers"], t["bias"], t["n"])
+            assert as_csr(E.infer(model, FeatureBatch(sm(t["y0"])))).identical(t["y"])
