@@ -78,6 +78,14 @@ __device__ __forceinline__ T bias_relu_clamp(T acc, T bias, T ymax) {
     const T c = v > ymax ? ymax : v;
     return (acc != T(0) && v > T(0)) ? c : T(0);  // selects, no branches
 }
+// The same, also reporting whether the entry is kept (stored): kept implies
+// a value in (0, ymax], so the live-row bit needs no second compare.
+template <typename T>
+__device__ __forceinline__ T bias_relu_clamp_keep(T acc, T bias, T ymax, bool& keep) {
+    const T v = Arith<T>::add(acc, bias);
+    keep = (acc != T(0)) & (v > T(0));  // NaN v: not kept, like engine.py:130
+    return keep ? fmin(v, ymax) : T(0);  // v > ymax -> ymax (one min instruction)
+}
 
 // engine.py:129-133 on one STORED entry (CSR path: stored means present).
 template <typename T>
@@ -174,23 +182,23 @@ __device__ __forceinline__ double ld_w(const double* p, uint64_t pol) {
 }
 
 // One live slot of a warp's compacted slot list: 16 bytes, read with one
-// 128-bit shared load per slot.
+// 128-bit shared load per slot (base and weight first, so the bit-line
+// gather, which needs no mask, reads them with one 64-bit load).
 template <typename T>
-struct __align__(16) SlotEntry {
+struct SlotEntry;
+template <>
+struct __align__(16) SlotEntry<float> {
     unsigned base;  // heap index of the line's first kept sector
+    float w;        // weight
     unsigned mask;  // lanes whose sector of that line is kept (nonzero)
-    T w;            // weight
+    unsigned pad;
 };
-template <typename T>
-__device__ __forceinline__ SlotEntry<T> load_entry(const SlotEntry<T>* e) {
-    const uint4 r = *reinterpret_cast<const uint4*>(e);
-    SlotEntry<T> o;
-    o.base = r.x;
-    o.mask = r.y;
-    if constexpr (sizeof(T) == 4) o.w = __uint_as_float(r.z);
-    else o.w = __hiloint2double((int)r.w, (int)r.z);
-    return o;
-}
+template <>
+struct __align__(16) SlotEntry<double> {
+    unsigned base;
+    unsigned mask;
+    double w;
+};
 
 template <typename T>
 struct LayerDesc {
@@ -645,13 +653,15 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
             // bits l*RPL .. l*RPL+RPL-1 (float: byte l; double: half of byte l/2)
             constexpr unsigned kMaskBits = (1u << RPL) - 1u;
             const int bpos = lane * RPL;
+            // padding entries (base 0, weight 0) read some byte of the tile's
+            // heap and add +0 to every chain: no guard needed
+            const unsigned char* inb = reinterpret_cast<const unsigned char*>(in) + (bpos >> 3);
+            asm("mov.b64 %0, %0;" : "+l"(inb));  // per-lane base: one wide multiply-add per address
             auto issue_b = [&](unsigned (&by)[GB], T (&wv)[GB], int i0) {
 #pragma unroll
                 for (int u = 0; u < GB; ++u) {
-                    const SlotEntry<T> e = load_entry(wlist + i0 + u);
-                    by[u] = e.mask ? ((unsigned)__ldg(reinterpret_cast<const unsigned char*>(in) +
-                                                      (size_t)e.base * 32 + (bpos >> 3)) >> (bpos & 7)) & kMaskBits
-                                   : 0u;
+                    const SlotEntry<T> e = wlist[i0 + u];
+                    by[u] = ((unsigned)__ldg(inb + (size_t)e.base * 32) >> (bpos & 7)) & kMaskBits;
                     wv[u] = e.w;
                 }
             };
@@ -676,7 +686,7 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
             auto issue = [&](T (&y)[GB][RPL], T (&wv)[GB], int i0) {
 #pragma unroll
                 for (int u = 0; u < GB; ++u) {
-                    const SlotEntry<T> e = load_entry(wlist + i0 + u);
+                    const SlotEntry<T> e = wlist[i0 + u];
                     const bool lv = (e.mask & lbit) != 0u;
                     const char* p = in + (size_t)(e.base + __popc(e.mask & below)) * 32;
                     if (ZFILL) {
@@ -715,11 +725,21 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
             cb = 0;
             T v[RPL];
             unsigned bits = 0u;
+            if (a.epilogue) {
 #pragma unroll
-            for (int c = 0; c < RPL; ++c) {
-                v[c] = a.epilogue ? bias_relu_clamp(acc[c], L.bias, a.ymax) : acc[c];
-                bits |= (v[c] != T(0)) ? (1u << c) : 0u;
-                acc[c] = T(0);
+                for (int c = 0; c < RPL; ++c) {
+                    bool keep;
+                    v[c] = bias_relu_clamp_keep(acc[c], L.bias, a.ymax, keep);
+                    bits |= keep ? (1u << c) : 0u;
+                    acc[c] = T(0);
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < RPL; ++c) {
+                    v[c] = acc[c];
+                    bits |= (v[c] != T(0)) ? (1u << c) : 0u;
+                    acc[c] = T(0);
+                }
             }
             const unsigned om = __ballot_sync(0xffffffffu, bits != 0u);
             unsigned hb = 0u;
