@@ -567,7 +567,6 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
     char* out = reinterpret_cast<char*>(odd ? a.slab[0] : a.slab[1]) + tile_lines * kLineBytes;
     const uint2* imeta = (odd ? a.meta[1] : a.meta[0]) + tile_lines;
     uint2* ometa = (odd ? a.meta[0] : a.meta[1]) + tile_lines;
-    uint32_t* heap_out = a.heap + (size_t)(l + 1) * a.n_tiles + t;
     const unsigned below = lbit - 1u;
     const int jw = j0 + warp;
     if (jw >= j1) return;
@@ -741,10 +740,11 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
                     acc[c] = T(0);
                 }
             }
+            // the column's kept sectors are packed at the front of its own
+            // 1 KB line slot: no heap allocation (a global atomic round trip
+            // per column was the largest single stall)
             const unsigned om = __ballot_sync(0xffffffffu, bits != 0u);
-            unsigned hb = 0u;
-            if (lane == 0 && om) hb = atomicAdd(heap_out, (unsigned)__popc(om));
-            hb = __shfl_sync(0xffffffffu, hb, 0);
+            const unsigned hb = (unsigned)cj * 32u;
             if (bits) st32(out + (size_t)(hb + __popc(om & below)) * 32, v);
             if (lane == 0) ometa[cj] = make_uint2(om, hb);
             alive_bits |= bits;
