@@ -60,7 +60,7 @@ def hbm_peak():
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -79,7 +79,10 @@ class ClockSampler:
         except Exception:  # noqa: BLE001
             self.proc = None
 
-    def stop(self):
+    def stop(self, window=None):
+        """Summarise the samples; with window=(t0, t1) (time.time() of the
+        timed region) only samples inside it count, unless none fell inside
+        (a very short region), then every sample taken under load counts."""
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -90,6 +93,20 @@ class ClockSampler:
         self.file.flush()
         rows = [ln.split(",") for ln in Path(self.file.name).read_text().splitlines() if ln.strip()]
         os.unlink(self.file.name)
+        scope = "all"
+        if window is not None:
+            import datetime
+
+            def ts(r):
+                try:
+                    return datetime.datetime.strptime(r[0].strip(), "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                except Exception:  # noqa: BLE001
+                    return None
+            inside = [r for r in rows if ts(r) is not None and window[0] <= ts(r) <= window[1]]
+            if inside:
+                rows, scope = inside, "timed region"
+            else:
+                scope = "warm-up + timed region (timed region shorter than the sampling period)"
         sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
         mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -102,7 +119,7 @@ class ClockSampler:
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(rows)}
+                "reasons": sorted(reasons), "samples": len(rows), "scope": scope}
 
 
 # ---------------------------------------------------------- distributed
@@ -126,6 +143,21 @@ def layer_bytes(w: W.Workload, elem: int, live: np.ndarray, nnz0: int, rows: int
         rd = nnz0 * (4 + elem) + (rows + 1) * 8 if l == 0 else elem * w.n * R
         out[l] = rd + elem * w.n * R + (4 + elem) * w.width * w.n
     return out
+
+
+def measured_traffic(w: W.Workload, rows: int, dtype: str, kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full
+    capture of this exact workload (profiles/traffic.json, written by
+    tools/traffic_json.py), or None when no capture matches."""
+    try:
+        d = json.loads((ROOT / "profiles" / "traffic.json").read_text())
+    except Exception:  # noqa: BLE001
+        return None
+    for e in d.get("captures", []):
+        if (e.get("kernel") == kernel and e.get("n") == w.n and e.get("rows") == rows
+                and e.get("dtype") == dtype and e.get("workload") == w.name and e.get("layers") == w.layers):
+            return {"bytes": float(e["dram_bytes"]), "source": e["source"]}
+    return None
 
 
 # ------------------------------------------------------------ CPU oracle
@@ -193,22 +225,26 @@ def run_ours(args, dist: RankGroup):
     batch = net.upload_csr(rows, off, cols, vals)
     setup_s = time.perf_counter() - t_setup
 
+    clocks = ClockSampler(dev)
+    clocks.start()  # before the warm-up, so nvidia-smi is sampling by the timed region
     for _ in range(args.warmup):
         net.run(batch, w.ymax)
     dist.barrier()
     torch.cuda.synchronize(dev)
-    clocks = ClockSampler(dev)
-    clocks.start()
+    t_region0 = time.time()
     dev_ms, wall0 = 0.0, time.perf_counter()
     launches = 0
+    stage_ms = np.zeros(3)
     for _ in range(args.steps):
         res = net.run(batch, w.ymax)
         dev_ms += res.device_ms
         launches += res.launches
+        stage_ms += res.stage_ms
     torch.cuda.synchronize(dev)
     wall_ms = (time.perf_counter() - wall0) * 1e3
+    t_region1 = time.time()
     dist.barrier()
-    clk = clocks.stop()
+    clk = clocks.stop((t_region0, t_region1))
     ms_per_step = dist.max(dev_ms / args.steps)
     wall_per_step = dist.max(wall_ms / args.steps)
     cats = dist.gather_categories(res.categories, r0)
@@ -220,24 +256,37 @@ def run_ours(args, dist: RankGroup):
     net.set_layer_timing(False)
     lb = layer_bytes(w, elem, prof.live_rows, nnz0, rows)
     live_layers = np.nonzero(prof.live_rows[:-1] > 0)[0]
-    dom = int(live_layers[np.argmax(prof.layer_ms[live_layers])]) if live_layers.size else 0
     peak, peak_kind = hbm_peak()
-    dom_gbs = lb[dom] / (prof.layer_ms[dom] * 1e-3) / 1e9 if prof.layer_ms[dom] > 0 else 0.0
     live_ms = float(prof.layer_ms[live_layers].sum()) if live_layers.size else 0.0
     all_gbs = lb.sum() / (live_ms * 1e-3) / 1e9 if live_ms > 0 else 0.0
+    # dominant launch of the timed steps (CUDA events on the engine's stream):
+    # the bit-line first-layer launch covers layer 1, the persistent launch
+    # the rest; its algorithmic bytes are those of the layers it ran
+    stage_ms = dist.max_array(stage_ms / args.steps)
+    bin_first = stage_ms[1] > 0
+    launch_bytes = [0.0, float(lb[0]) if bin_first else 0.0, float(lb[1:].sum() if bin_first else lb.sum())]
+    names = ["densify_kernel (Y0 -> tiles)", "bin_layer_kernel (layer 1, bit-line tiles)",
+             f"net_kernel (layers {2 if bin_first else 1}-{w.layers}, persistent)"]
+    dom = int(np.argmax(stage_ms))
+    dom_gbs = launch_bytes[dom] / (stage_ms[dom] * 1e-3) / 1e9 if stage_ms[dom] > 0 else 0.0
+    traffic = measured_traffic(w, rows, args.dtype, names[dom].split()[0])
 
     # end to end through the C ABI with host buffers: H2D of Y0 + run + D2H
     e2e_ms = 0.0
+    e2e_split = []
     for i in range(args.steps + 1):
         t0 = time.perf_counter()
         b2 = net.upload_csr(rows, off, cols, vals)
+        t1 = time.perf_counter()
         r2 = net.run(b2, w.ymax)
         _ = r2.categories.copy()
-        dt = (time.perf_counter() - t0) * 1e3
+        t2 = time.perf_counter()
+        dt = (t2 - t0) * 1e3
         h2d_step = b2.h2d_bytes
         b2.close()
         if i > 0:  # first call grows the pinned staging buffer
             e2e_ms += dt
+            e2e_split.append((round((t1 - t0) * 1e3, 1), round((t2 - t1) * 1e3, 1)))
     e2e_ms = dist.max(e2e_ms / args.steps)
     h2d = h2d_step
     d2h = (w.layers + 1) * 4 + int(r2.live_rows[-1]) * 4
@@ -274,11 +323,14 @@ def run_ours(args, dist: RankGroup):
             "peak": peak,
             "unit": "GB/s",
             "frac": dom_gbs / peak,
-            "traffic": None,
-            "kernel": f"layer_kernel layer {dom + 1} (R={int(prof.live_rows[dom])})",
-            "per_launch_ms": float(prof.layer_ms[dom]),
-            "algorithmic_bytes": float(lb[dom]),
-            "all_live_launches_gbs": all_gbs,
+            "traffic": traffic["bytes"] if traffic else None,
+            "traffic_source": traffic["source"] if traffic else None,
+            "kernel": names[dom],
+            "per_launch_ms": float(stage_ms[dom]),
+            "algorithmic_bytes": launch_bytes[dom],
+            "launch_ms": {"densify": round(float(stage_ms[0]), 3), "bin_layer": round(float(stage_ms[1]), 3),
+                          "net": round(float(stage_ms[2]), 3)},
+            "all_live_layers_gbs": all_gbs,
             "live_layer_ms": [round(float(prof.layer_ms[l]), 3) for l in live_layers[:8]],
             "peak_kind": peak_kind,
         },
@@ -288,6 +340,7 @@ def run_ours(args, dist: RankGroup):
             "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h,
             "ms_per_step": e2e_ms,
+            "upload_run_ms_per_step": e2e_split[:8],
         },
         "gpu_launches": launches,
         "wall_ms_per_step": wall_per_step,
@@ -412,7 +465,7 @@ def workload(args) -> W.Workload:
 def main(argv=None):
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--workload", default="C4", choices=sorted(W.CONFIGS))

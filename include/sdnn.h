@@ -121,6 +121,12 @@ int sdnn_result_live_rows(const sdnn_result *r, int64_t *live_rows);
 int sdnn_net_set_layer_timing(sdnn_net *net, int on);
 /* Per-layer device milliseconds of a run made with layer timing on. */
 int sdnn_result_layer_ms(const sdnn_result *r, double *ms);
+/* Device milliseconds of the run's launches, from CUDA events recorded on
+ * the engine's stream in every run: ms[0] = Y0 expansion into tiles
+ * (densify), ms[1] = the first layer's own launch over bit-line tiles (0
+ * when Y0 is not binary), ms[2] = the persistent launch over the remaining
+ * layers. */
+int sdnn_result_stage_ms(const sdnn_result *r, double *ms);
 /* Kernel launches the run issued (evidence for bench gpu_launches). */
 int sdnn_result_launches(const sdnn_result *r, int64_t *n);
 /* Final Y as canonical CSR (ascending columns, no zeros) widened to

@@ -47,6 +47,7 @@ SIGNATURES = [
     ("sdnn_result_live_rows", cint, [vp, vp]),
     ("sdnn_net_set_layer_timing", cint, [vp, cint]),
     ("sdnn_result_layer_ms", cint, [vp, vp]),
+    ("sdnn_result_stage_ms", cint, [vp, vp]),
     ("sdnn_result_launches", cint, [vp, P(i64)]),
     ("sdnn_result_y_nnz", cint, [vp, P(i64)]),
     ("sdnn_result_y_csr", cint, [vp, vp, vp, vp]),

@@ -107,6 +107,7 @@ struct sdnn_net {
     int64_t descs_n = 0;    // layers mirrored in `descs`
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev_d = nullptr, ev_b = nullptr;  // after densify, after the bit-line layer
     // run scratch, grown on demand
     void* slab[2] = {nullptr, nullptr};
     uint2* meta[2] = {nullptr, nullptr};
@@ -151,6 +152,7 @@ struct sdnn_result {
     double dev_ms = 0, wall_ms = 0;
     int64_t launches = 0;
     std::vector<double> layer_ms;  // per layer, when layer timing is on
+    double stage_ms[3] = {0, 0, 0};  // densify, first (bit-line) layer launch, persistent layer launch
     bool have_y = false;
     std::vector<int64_t> off, cols;
     std::vector<double> vals;
@@ -513,6 +515,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
         CK(cudaGetLastError());
         res->launches += 1;
     }
+    CK(cudaEventRecord(net->ev_d, net->stream));
     if (a.bin_in) {  // layer 1 over bit-line tiles: its own launch
         const void* bfn = (const void*)bin_layer_kernel<T>;
         CK(cudaFuncSetAttribute(bfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -523,12 +526,15 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
         res->launches += 1;
         a.first_l = 1;
     }
-    if (a.first_l < a.L)
+    CK(cudaEventRecord(net->ev_b, net->stream));
+    if (a.first_l < a.L) {
         CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, smem, net->stream));
+        res->launches += 1;
+    }
     CK(cudaEventRecord(net->ev1, net->stream));
-    res->launches += 1;
     live_rows_kernel<<<(unsigned)(nl + 1), 256, 0, net->stream>>>(net->alive, (int)tiles1, AW, live);
     CK(cudaGetLastError());
+    res->launches += 1;
     std::vector<int64_t> lr(nl + 1);
     std::vector<unsigned long long> st(nl + 1);
     std::vector<uint32_t> alive_last(tiles1 * AW);
@@ -542,6 +548,15 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, net->ev0, net->ev1));
     dev_ms += ms;
+    {
+        float m0 = 0, m1 = 0, m2 = 0;
+        CK(cudaEventElapsedTime(&m0, net->ev0, net->ev_d));
+        CK(cudaEventElapsedTime(&m1, net->ev_d, net->ev_b));
+        CK(cudaEventElapsedTime(&m2, net->ev_b, net->ev1));
+        res->stage_ms[0] += m0;
+        res->stage_ms[1] += m1;
+        res->stage_ms[2] += m2;
+    }
     for (int64_t l = 0; l <= nl; ++l) res->live[l] += lr[l];
     if (net->layer_timing)
         for (int64_t l = 0; l < nl; ++l)
@@ -753,6 +768,8 @@ int make_net(int device, int dtype, int64_t n, sdnn_net** out) {
     }
     CK(cudaEventCreate(&net->ev0));
     CK(cudaEventCreate(&net->ev1));
+    CK(cudaEventCreate(&net->ev_d));
+    CK(cudaEventCreate(&net->ev_b));
     *out = net;
     return SDNN_OK;
 }
@@ -808,6 +825,8 @@ void sdnn_net_destroy(sdnn_net* net) {
         if (e) cudaEventDestroy(e);
     if (net->ev0) cudaEventDestroy(net->ev0);
     if (net->ev1) cudaEventDestroy(net->ev1);
+    if (net->ev_d) cudaEventDestroy(net->ev_d);
+    if (net->ev_b) cudaEventDestroy(net->ev_b);
     if (net->stream) cudaStreamDestroy(net->stream);
     delete net;
 }
@@ -975,6 +994,12 @@ int sdnn_result_live_rows(const sdnn_result* r, int64_t* live) {
 int sdnn_net_set_layer_timing(sdnn_net* net, int on) {
     if (!net) return fail(SDNN_ERR_PARAMETER, "null argument");
     net->layer_timing = on;
+    return SDNN_OK;
+}
+
+int sdnn_result_stage_ms(const sdnn_result* r, double* ms) {
+    if (!r || !ms) return fail(SDNN_ERR_PARAMETER, "null argument");
+    for (int i = 0; i < 3; ++i) ms[i] = r->stage_ms[i];
     return SDNN_OK;
 }
 

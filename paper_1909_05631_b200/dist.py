@@ -61,6 +61,18 @@ class RankGroup:
         self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
         return float(t.item())
 
+    def max_array(self, x):
+        """Elementwise max over ranks of a small float array."""
+        import numpy as np
+
+        x = np.asarray(x, dtype=np.float64)
+        if self.td is None:
+            return x
+        dev = f"cuda:{self.local}" if self.backend == "nccl" else "cpu"
+        t = self.torch.tensor(x, dtype=self.torch.float64, device=dev)
+        self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
+        return t.cpu().numpy()
+
     def sum(self, x: float) -> float:
         if self.td is None:
             return float(x)

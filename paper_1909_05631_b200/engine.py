@@ -149,6 +149,7 @@ class RunResult:
     launches: int
     y: tuple | None = None      # (off, cols, vals) float64 CSR, when requested
     layer_ms: np.ndarray | None = None  # per layer, when layer timing is on
+    stage_ms: np.ndarray | None = None  # [densify, bit-line layer launch, persistent launch]
 
 
 class DeviceBatch:
@@ -301,6 +302,8 @@ def _collect(h, n_rows: int, want_y: bool) -> RunResult:
         layer_ms = layer_ms[:nl.value]
     else:
         layer_ms = None
+    stage_ms = np.zeros(3)
+    _lib.check(L.sdnn_result_stage_ms(h, _lib.ptr(stage_ms)))
     y = None
     if want_y:
         nnz = ctypes.c_int64()
@@ -311,7 +314,7 @@ def _collect(h, n_rows: int, want_y: bool) -> RunResult:
         _lib.check(L.sdnn_result_y_csr(h, _lib.ptr(off), _lib.ptr(cols), _lib.ptr(vals)))
         y = (off, cols[:nnz.value], vals[:nnz.value])
     return RunResult(cats, live, L.sdnn_result_device_ms(h), L.sdnn_result_wall_ms(h),
-                     launches.value, y, layer_ms)
+                     launches.value, y, layer_ms, stage_ms)
 
 
 # ------------------------------------------------------- network residency

@@ -33,9 +33,10 @@ def _worker(rank, world, port, q):
     cats = g.gather_categories(O.categorize(out), r0)
     slowest = g.max(float(rank + 1))
     total = g.sum(float(r1 - r0))
+    stages = g.max_array(np.array([rank, 10.0 - rank, 3.0]))
     g.barrier()
     if rank == 0:
-        q.put((cats.tolist(), slowest, total))
+        q.put((cats.tolist(), slowest, total, stages.tolist()))
     g.close()
 
 
@@ -57,7 +58,7 @@ def test_two_rank_gloo_matches_single_process():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    cats, slowest, total = q.get(timeout=240)
+    cats, slowest, total, stages = q.get(timeout=240)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -67,3 +68,4 @@ def test_two_rank_gloo_matches_single_process():
     want = O.categorize(O.infer(layers, [w.bias] * w.layers, O.CSR(w.batch, w.n, off, cols, vals)))
     assert cats == want.tolist() and len(cats) > 0
     assert slowest == 2.0 and total == w.batch
+    assert stages == [1.0, 10.0, 3.0]  # per-launch times: elementwise max over ranks
