@@ -119,9 +119,15 @@ struct sdnn_net {
     int64_t rcap = 0;
     uint32_t* alive = nullptr;
     int64_t acap = 0;
+    int32_t* rowid_buf = nullptr;  // per-run scratch below: grown, never freed per run
+    int64_t idcap = 0;
     int32_t* tile_count = nullptr;
     int64_t* live_rows = nullptr;
     unsigned long long* stamps = nullptr;
+    uint32_t* heap = nullptr;
+    unsigned* work = nullptr;
+    int64_t lcap = 0;  // layers + 1 the per-layer scratch holds
+    int64_t hcap = 0;  // heap counters
     unsigned* bar = nullptr;
     int32_t* n_sel = nullptr;
     int64_t ccap = 0;
@@ -420,17 +426,25 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     CK(cudaStreamSynchronize(net->stream));
     const int64_t n_tiles = (n_live + TR - 1) / TR;
     if (int rc = ensure_tiles(net, n_tiles, ld)) return rc;
-    CK(cudaMalloc(&net->rowid, std::max<int64_t>(n_tiles * TR, 1) * 4));
+    if (int rc = grow(net->rowid_buf, net->idcap, std::max<int64_t>(n_tiles * TR, 1), 4)) return rc;
+    net->rowid = net->rowid_buf;
     CK(cudaMemsetAsync(net->rowid, 0xff, std::max<int64_t>(n_tiles * TR, 1) * 4, net->stream));
     if (n_live) CK(cudaMemcpyAsync(net->rowid, net->rowlist, n_live * 4, cudaMemcpyDeviceToDevice, net->stream));
     const int64_t tiles1 = std::max<int64_t>(n_tiles, 1);
     if (int rc = grow(net->alive, net->acap, (nl + 1) * tiles1 * AW, 4)) return rc;
-    int32_t* tile_count = nullptr;
-    int64_t* live = nullptr;
-    unsigned long long* stamps = nullptr;
-    CK(cudaMalloc(&tile_count, (nl + 1) * 4));
-    CK(cudaMalloc(&live, (nl + 1) * 8));
-    CK(cudaMalloc(&stamps, (nl + 1) * 8));
+    // per-layer scratch (no cudaMalloc/cudaFree per run: both synchronise
+    // and made back-to-back runs stall for hundreds of ms)
+    if (nl + 1 > net->lcap) {
+        int64_t c1 = 0, c2 = 0, c3 = 0, c4 = 0;
+        if (int rc = grow(net->tile_count, c1, nl + 1, 4)) return rc;
+        if (int rc = grow(net->live_rows, c2, nl + 1, 8)) return rc;
+        if (int rc = grow(net->stamps, c3, nl + 1, 8)) return rc;
+        if (int rc = grow(net->work, c4, nl + 1, 4)) return rc;
+        net->lcap = nl + 1;
+    }
+    int32_t* tile_count = net->tile_count;
+    int64_t* live = net->live_rows;
+    unsigned long long* stamps = net->stamps;
     if (!net->bar) CK(cudaMalloc(&net->bar, 8));
     CK(cudaMemsetAsync(net->alive, 0, (nl + 1) * tiles1 * AW * 4, net->stream));
     CK(cudaMemsetAsync(tile_count, 0, (nl + 1) * 4, net->stream));
@@ -440,11 +454,10 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
         CK(cudaMalloc(&net->zero, 64));
         CK(cudaMemset(net->zero, 0, 64));
     }
-    uint32_t* heap = nullptr;
-    CK(cudaMalloc(&heap, (nl + 1) * tiles1 * 4));
+    if (int rc = grow(net->heap, net->hcap, (nl + 1) * tiles1, 4)) return rc;
+    uint32_t* heap = net->heap;
     CK(cudaMemsetAsync(heap, 0, (nl + 1) * tiles1 * 4, net->stream));
-    unsigned* work = nullptr;
-    CK(cudaMalloc(&work, std::max<int64_t>(nl, 1) * 4));
+    unsigned* work = net->work;
     CK(cudaMemsetAsync(work, 0, std::max<int64_t>(nl, 1) * 4, net->stream));
 
     NetArgs<T> a{};
@@ -572,13 +585,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
             return rc;
         pieces.push_back(std::move(p));
     }
-    cudaFree(tile_count);
-    cudaFree(live);
-    cudaFree(stamps);
-    cudaFree(work);
-    cudaFree(heap);
-    cudaFree(net->rowid);
-    net->rowid = nullptr;
+
     return SDNN_OK;
 }
 
@@ -813,8 +820,12 @@ void sdnn_net_destroy(sdnn_net* net) {
         cudaFree(net->meta[b]);
     }
     cudaFree(net->zero);
-    cudaFree(net->rowid);
+    cudaFree(net->rowid_buf);
     cudaFree(net->rowlist);
+    cudaFree(net->live_rows);
+    cudaFree(net->stamps);
+    cudaFree(net->heap);
+    cudaFree(net->work);
     cudaFree(net->alive);
     cudaFree(net->tile_count);
     cudaFree(net->bar);
