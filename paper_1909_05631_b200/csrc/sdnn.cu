@@ -137,6 +137,11 @@ struct sdnn_net {
     size_t pinned_cap = 0;
     cudaEvent_t stage_ev[2] = {nullptr, nullptr};
     int layer_timing = 0;
+    // weight-ingest scratch (CSR -> ELL on the device), grown on demand
+    void* ing_pinned = nullptr;
+    size_t ing_pinned_cap = 0;
+    void* ing_dev = nullptr;
+    size_t ing_dev_cap = 0;
 };
 
 struct sdnn_batch {
@@ -719,34 +724,124 @@ void free_batch(sdnn_batch* b) {
 
 // CSR by input row (reference LayerWeights) -> output-major ELL, inputs
 // ascending per output (rows are visited in ascending order).
-int csr_to_ell(int64_t n_in, int64_t n_out, const int64_t* off, const int64_t* cols,
-               const double* vals, int64_t nnz, std::vector<int32_t>& idx,
-               std::vector<double>& val, int& width, std::vector<int64_t>& degree) {
-    if (off[0] != 0 || off[n_in] != nnz) return fail(SDNN_ERR_PARAMETER, "inconsistent weight offsets");
-    std::vector<int64_t> deg(n_out + 1, 0);
-    for (int64_t i = 0; i < n_in; ++i) {
+// CSR by input -> device ELL by output (weight ingest).
+// Host: validate offsets, narrow columns to int32 and values to T into a
+// pinned buffer (threads), one H2D.  Device: entry rows, column check and
+// degrees, stable radix sort by column, degree scan, max degree, ELL fill.
+// Errors as the reference raises them: bad offsets / columns -> parameter.
+template <typename T>
+int ingest_csr(sdnn_net* net, int64_t n_in, int64_t n_out, const int64_t* off, const int64_t* cols,
+               const double* vals, double bias) {
+    if (off[0] != 0) return fail(SDNN_ERR_PARAMETER, "inconsistent weight offsets");
+    for (int64_t i = 0; i < n_in; ++i)
         if (off[i + 1] < off[i]) return fail(SDNN_ERR_PARAMETER, "weight offsets non-monotone");
-        for (int64_t p = off[i]; p < off[i + 1]; ++p) {
-            if (cols[p] < 0 || cols[p] >= n_out)
-                return fail(SDNN_ERR_PARAMETER, "weight column %lld out of range", (long long)cols[p]);
-            deg[cols[p]]++;
-        }
+    const int64_t nnz = off[n_in];
+    if (nnz >= (1LL << 31) || n_out >= (1LL << 31))
+        return fail(SDNN_ERR_CAPACITY, "layer with %lld entries exceeds int32 indexing", (long long)nnz);
+    const int64_t nz = std::max<int64_t>(nnz, 1);
+    const bool timing = env_int("SDNN_INGEST_TIMING", 0) != 0;
+    double t_prev = now_ms();
+    auto lap = [&](const char* what) {
+        if (!timing) return;
+        const double t = now_ms();
+        fprintf(stderr, "ingest %-12s %8.2f ms\n", what, t - t_prev);
+        t_prev = t;
+    };
+    // pinned: offsets (int64), columns (int32), values (T)
+    const size_t pin_bytes = (size_t)(n_in + 1) * 8 + (size_t)nz * (4 + sizeof(T));
+    if (pin_bytes > net->ing_pinned_cap) {
+        if (net->ing_pinned) CK(cudaFreeHost(net->ing_pinned));
+        net->ing_pinned = nullptr;
+        CK(cudaMallocHost(&net->ing_pinned, pin_bytes));
+        net->ing_pinned_cap = pin_bytes;
     }
-    int64_t w = 0;
-    for (int64_t j = 0; j < n_out; ++j) w = std::max(w, deg[j]);
-    width = (int)w;
-    idx.assign((size_t)n_out * w, 0);
-    val.assign((size_t)n_out * w, 0.0);
-    std::vector<int64_t> fill(n_out, 0);
-    degree.assign(deg.begin(), deg.begin() + n_out);
-    for (int64_t i = 0; i < n_in; ++i) {
-        for (int64_t p = off[i]; p < off[i + 1]; ++p) {
-            const int64_t j = cols[p];
-            const size_t e = (size_t)j * w + fill[j]++;
-            idx[e] = (int32_t)i;
-            val[e] = vals[p];
+    char* hp = reinterpret_cast<char*>(net->ing_pinned);
+    int64_t* h_off = reinterpret_cast<int64_t*>(hp);
+    int32_t* h_cols = reinterpret_cast<int32_t*>(hp + (size_t)(n_in + 1) * 8);
+    T* h_vals = reinterpret_cast<T*>(hp + (size_t)(n_in + 1) * 8 + (size_t)nz * 4);
+    std::memcpy(h_off, off, (size_t)(n_in + 1) * 8);
+    parallel_for(nnz, [&](int64_t a, int64_t b) {
+        for (int64_t p = a; p < b; ++p) {
+            const int64_t c = cols[p];
+            h_cols[p] = (c < 0 || c >= n_out) ? -1 : (int32_t)c;  // flagged on the device
+            h_vals[p] = (T)vals[p];
         }
+    });
+    lap("host narrow");
+    // device scratch: off, cols, keys_out, perm_in, perm_out, rowid, vals, deg, start, flags, cub temp
+    size_t sort_bytes = 0, scan_bytes = 0, max_bytes = 0;
+    int end_bit = 1;
+    while ((1LL << end_bit) < n_out) ++end_bit;
+    cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                    (const int32_t*)nullptr, (int32_t*)nullptr, (int)nz, 0, end_bit, net->stream);
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (const int32_t*)nullptr, (int32_t*)nullptr, (int)n_out,
+                                  net->stream);
+    cub::DeviceReduce::Max(nullptr, max_bytes, (const int32_t*)nullptr, (int32_t*)nullptr, (int)n_out, net->stream);
+    auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+    const size_t o_off = 0, o_cols = o_off + al((size_t)(n_in + 1) * 8), o_keys = o_cols + al((size_t)nz * 4),
+                 o_pin = o_keys + al((size_t)nz * 4), o_pout = o_pin + al((size_t)nz * 4),
+                 o_row = o_pout + al((size_t)nz * 4), o_vals = o_row + al((size_t)nz * 4),
+                 o_deg = o_vals + al((size_t)nz * sizeof(T)), o_start = o_deg + al((size_t)n_out * 4),
+                 o_flag = o_start + al((size_t)n_out * 4), o_tmp = o_flag + 256,
+                 total = o_tmp + al(std::max(sort_bytes, std::max(scan_bytes, max_bytes)));
+    if (total > net->ing_dev_cap) {
+        if (net->ing_dev) CK(cudaFree(net->ing_dev));
+        net->ing_dev = nullptr;
+        CK(cudaMalloc(&net->ing_dev, total));
+        net->ing_dev_cap = total;
     }
+    char* d = reinterpret_cast<char*>(net->ing_dev);
+    int64_t* d_off = reinterpret_cast<int64_t*>(d + o_off);
+    int32_t* d_cols = reinterpret_cast<int32_t*>(d + o_cols);
+    int32_t* d_keys = reinterpret_cast<int32_t*>(d + o_keys);
+    int32_t* d_pin = reinterpret_cast<int32_t*>(d + o_pin);
+    int32_t* d_pout = reinterpret_cast<int32_t*>(d + o_pout);
+    int32_t* d_row = reinterpret_cast<int32_t*>(d + o_row);
+    T* d_vals = reinterpret_cast<T*>(d + o_vals);
+    int32_t* d_deg = reinterpret_cast<int32_t*>(d + o_deg);
+    int32_t* d_start = reinterpret_cast<int32_t*>(d + o_start);
+    int* d_flag = reinterpret_cast<int*>(d + o_flag);  // [0] bad column, [1] max degree
+    void* d_tmp = d + o_tmp;
+    cudaStream_t st = net->stream;
+    CK(cudaMemcpyAsync(d_off, h_off, (size_t)(n_in + 1) * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_cols, h_cols, (size_t)nnz * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_vals, h_vals, (size_t)nnz * sizeof(T), cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(d_deg, 0, (size_t)n_out * 4, st));
+    CK(cudaMemsetAsync(d_flag, 0, 8, st));
+    const int grid = net->sm_count * 8;
+    if (nnz) {
+        csr_rowid_kernel<<<grid, 256, 0, st>>>(d_off, n_in, d_row);
+        csr_degree_kernel<<<grid, 256, 0, st>>>(d_cols, nnz, n_out, d_deg, d_pin, d_flag);
+        CK(cudaGetLastError());
+        CK(cub::DeviceRadixSort::SortPairs(d_tmp, sort_bytes, d_cols, d_keys, d_pin, d_pout, (int)nnz, 0, end_bit,
+                                           st));
+    }
+    CK(cub::DeviceScan::ExclusiveSum(d_tmp, scan_bytes, d_deg, d_start, (int)n_out, st));
+    CK(cub::DeviceReduce::Max(d_tmp, max_bytes, d_deg, d_flag + 1, (int)n_out, st));
+    int flags[2] = {0, 0};
+    CK(cudaMemcpyAsync(flags, d_flag, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    lap("h2d+sort");
+    if (flags[0]) return fail(SDNN_ERR_PARAMETER, "weight column out of range [0, %lld)", (long long)n_out);
+    DevLayer L;
+    L.width = flags[1];
+    L.wp = (L.width + 31) / 32 * 32;
+    L.bias = bias;
+    const size_t slots = (size_t)L.wp * (size_t)n_out;
+    CK(cudaMalloc(&L.idx, std::max<size_t>(slots, 1) * sizeof(int32_t)));
+    CK(cudaMalloc(&L.val, std::max<size_t>(slots, 1) * sizeof(T)));
+    lap("alloc");
+    CK(cudaMemsetAsync(L.idx, 0xff, slots * sizeof(int32_t), st));  // padding: index -1
+    CK(cudaMemsetAsync(L.val, 0, slots * sizeof(T), st));            // weight 0
+    if (nnz) {
+        ell_fill_kernel<T><<<grid, 256, 0, st>>>(d_keys, d_pout, d_start, d_row, d_vals, nnz, L.wp, L.idx,
+                                                 reinterpret_cast<T*>(L.val));
+        CK(cudaGetLastError());
+    }
+    CK(cudaStreamSynchronize(st));
+    lap("fill");
+    L.bytes = (int64_t)slots * (4 + (int64_t)sizeof(T));
+    net->layers.push_back(L);
     return SDNN_OK;
 }
 
@@ -832,6 +927,8 @@ void sdnn_net_destroy(sdnn_net* net) {
     cudaFree(net->n_sel);
     cudaFree(net->cub_tmp);
     if (net->pinned) cudaFreeHost(net->pinned);
+    if (net->ing_pinned) cudaFreeHost(net->ing_pinned);
+    cudaFree(net->ing_dev);
     for (auto e : net->stage_ev)
         if (e) cudaEventDestroy(e);
     if (net->ev0) cudaEventDestroy(net->ev0);
@@ -846,12 +943,9 @@ int sdnn_net_add_layer_csr(sdnn_net* net, const int64_t* w_off, const int64_t* w
                            const double* w_vals, int64_t nnz, double bias) {
     if (!net || !w_off) return fail(SDNN_ERR_PARAMETER, "null argument");
     if (int rc = set_device(net)) return rc;
-    std::vector<int32_t> idx;
-    std::vector<double> val;
-    std::vector<int64_t> deg;
-    int width = 0;
-    if (int rc = csr_to_ell(net->n, net->n, w_off, w_cols, w_vals, nnz, idx, val, width, deg)) return rc;
-    return upload_layer(net, net->n, width, idx.data(), val.data(), 0.0, bias, deg.data());
+    if (w_off[net->n] != nnz) return fail(SDNN_ERR_PARAMETER, "inconsistent weight offsets");
+    return net->dtype == SDNN_F64 ? ingest_csr<double>(net, net->n, net->n, w_off, w_cols, w_vals, bias)
+                                  : ingest_csr<float>(net, net->n, net->n, w_off, w_cols, w_vals, bias);
 }
 
 int sdnn_net_add_layer_ell(sdnn_net* net, int32_t width, const int32_t* idx, const double* vals,
@@ -1057,13 +1151,9 @@ int sdnn_spmm(int device, int dtype, int64_t n_rows, int64_t n_inner, int64_t n_
     sdnn_batch* b = nullptr;
     sdnn_result* res = nullptr;
     do {
-        std::vector<int32_t> idx;
-        std::vector<double> val;
-        std::vector<int64_t> deg;
-        int width = 0;
-        const int64_t nnz_w = w_off[n_inner];
-        if ((rc = csr_to_ell(n_inner, n_out, w_off, w_cols, w_vals, nnz_w, idx, val, width, deg))) break;
-        if ((rc = upload_layer(net, n_out, width, idx.data(), val.data(), 0.0, 0.0, deg.data()))) break;
+        rc = dtype == SDNN_F64 ? ingest_csr<double>(net, n_inner, n_out, w_off, w_cols, w_vals, 0.0)
+                               : ingest_csr<float>(net, n_inner, n_out, w_off, w_cols, w_vals, 0.0);
+        if (rc) break;
         b = new sdnn_batch;
         b->net = net;
         static const int64_t zero_off[1] = {0};

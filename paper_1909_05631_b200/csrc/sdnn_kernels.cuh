@@ -920,6 +920,51 @@ __global__ void extract_kernel(const T* __restrict__ slab, const uint2* __restri
     }
 }
 
+// ------------------------------------------------------------ weight ingest
+// CSR by input (the reference's LayerWeights, model.py:128-139) -> ELL by
+// output on the device.  The host only narrows the
+// columns to int32 and the values to T; the device writes every entry's row,
+// stable-radix-sorts the entries by column (CSR order is ascending by row,
+// so each column's entries stay ascending: one ordered chain per output, as
+// engine._spmm_kernel accumulates them), counts column degrees and fills the
+// padded ELL.
+
+// entry -> its input row (one warp per row)
+__global__ void csr_rowid_kernel(const int64_t* __restrict__ off, int64_t n_in, int32_t* __restrict__ rowid) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n_in; i += warps)
+        for (int64_t p = off[i] + lane; p < off[i + 1]; p += 32) rowid[p] = (int32_t)i;
+}
+
+// column range check + degree count; perm = 0..nnz-1 (the sort's payload)
+__global__ void csr_degree_kernel(const int32_t* __restrict__ cols, int64_t nnz, int64_t n_out,
+                                  int32_t* __restrict__ deg, int32_t* __restrict__ perm, int* bad) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t c = cols[p];
+        perm[p] = (int32_t)p;
+        if (c < 0 || c >= n_out) {
+            *bad = 1;
+            continue;
+        }
+        atomicAdd(&deg[c], 1);
+    }
+}
+
+// sorted position q -> slot q - start[col] of column col
+template <typename T>
+__global__ void ell_fill_kernel(const int32_t* __restrict__ skeys, const int32_t* __restrict__ sperm,
+                                const int32_t* __restrict__ start, const int32_t* __restrict__ rowid,
+                                const T* __restrict__ vals, int64_t nnz, int wp, int32_t* __restrict__ idx,
+                                T* __restrict__ val) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nnz; q += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t j = skeys[q], p = sperm[q];
+        const size_t e = (size_t)j * wp + (size_t)(q - start[j]);
+        idx[e] = rowid[p];
+        val[e] = vals[p];
+    }
+}
+
 // ---------------------------------------------------- CSR bias/ReLU/clamp
 // engine.apply_bias_relu_clamp on CSR values: count, then ordered write.
 __device__ __forceinline__ int block_prefix(bool flag, int* s_warp, int* total) {

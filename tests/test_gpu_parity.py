@@ -401,3 +401,40 @@ def test_zero_fill_and_keep_gathers_agree(env):
         for t in goldens.general()[:16]:
             model = model_of(t["layers"], t["bias"], t["n"])
             assert as_csr(E.infer(model, FeatureBatch(sm(t["y0"])))).identical(t["y"])
+
+
+def test_device_weight_ingest_general_csr():
+    """CSR -> ELL on the device (sort by column, ascending rows kept): column
+    degrees 0..~70 (padded ELL of 96 slots, several batches per column),
+    empty rows and columns, mixed signs; bit-exact against the oracle."""
+    rng = np.random.default_rng(21)
+    n = 300
+    dense = np.zeros((n, n))
+    for j in range(n):
+        deg = int(rng.integers(0, 71)) if j % 7 else 0
+        rows = rng.choice(n, size=deg, replace=False)
+        dense[rows, j] = rng.uniform(-0.4, 0.6, size=deg)
+    dense[5, :] = 0.0  # an empty input row
+    layers = [O.CSR.from_dense(dense), O.CSR.from_dense(dense.T.copy())]
+    y = np.where(rng.random((400, n)) < 0.2, rng.uniform(0.1, 2.0, (400, n)), 0.0)
+    y0 = O.CSR.from_dense(y)
+    bias = [-0.05, 0.1]
+    for dtype, prec in (("f64", 64), ("f32", 32)):
+        net = E.DeviceNetwork(n, 0, dtype)
+        for lw, b in zip(layers, bias):
+            net.add_layer_csr(sm(lw), b)
+        res = net.run(net.upload_csr(y0.n_rows, y0.off, y0.cols, y0.vals), 32.0, want_y=True)
+        want = O.infer(layers, bias, y0, precision=prec, threads=4)
+        assert O.CSR(y0.n_rows, n, *res.y).identical(want)
+        net.close()
+
+
+def test_device_weight_ingest_rejects_bad_csr():
+    net = E.DeviceNetwork(4, 0, "f64")
+    bad_col = SparseMatrix(4, 4, np.array([0, 1, 1, 1, 1]), np.array([4]), np.array([1.0]), check=False)
+    with pytest.raises(ParameterError):
+        net.add_layer_csr(bad_col, 0.0)
+    bad_off = SparseMatrix(4, 4, np.array([0, 2, 1, 2, 2]), np.array([0, 1]), np.array([1.0, 1.0]), check=False)
+    with pytest.raises(ParameterError):
+        net.add_layer_csr(bad_off, 0.0)
+    net.close()
