@@ -772,6 +772,179 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
         publish_alive<T>(a.alive + ((size_t)(l + 1) * a.n_tiles + t) * AW, alive_bits, &a.tile_count[l + 1]);
 }
 
+// ------------------------------------------ layer 1, two bit-line tiles per item
+// The first layer (binary Y0) is issue-bound and 43 % of its instructions are
+// per column (slot prefetch, compaction, loop control), so a warp computes
+// each output column for two tiles at once: one slot list, one entry load
+// {base A, base B, w A, w B} per slot, two byte loads, 16 predicated adds.
+// A line dead in one tile gets weight 0 there (its byte is read from some
+// valid sector and adds +0).  Bit-lines are 32 bytes, so two tiles in flight
+// stay small in L2 (unlike the float layers, where this halves L2 hit rate).
+struct __align__(16) BinEntry2 {
+    unsigned baseA, baseB;  // heap sector of the line in tile A / tile B
+    float wA, wB;           // weight, or 0 where the line is dead
+};
+static_assert(sizeof(BinEntry2) == sizeof(SlotEntry<float>), "slot lists share storage");
+
+template <int GB>
+__device__ __forceinline__ void bin_item2(const NetArgs<float>& a, const LayerDesc<float>& L, int tA, int tB,
+                                          int j0, int j1, BinEntry2* wlist) {
+    constexpr int RPL = 8, AW = alive_words<float>();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lbit = 1u << lane, below = lbit - 1u;
+    const bool hasB = tB >= 0;
+    const size_t linesA = (size_t)tA * a.ld, linesB = (size_t)(hasB ? tB : tA) * a.ld;
+    const unsigned char* inbA = reinterpret_cast<const unsigned char*>(a.slab[0]) + linesA * kLineBytes + lane;
+    const unsigned char* inbB = reinterpret_cast<const unsigned char*>(a.slab[0]) + linesB * kLineBytes + lane;
+    asm("mov.b64 %0, %0;" : "+l"(inbA));
+    asm("mov.b64 %0, %0;" : "+l"(inbB));
+    const uint2* imetaA = a.meta[0] + linesA;
+    const uint2* imetaB = a.meta[0] + linesB;
+    const int jw = j0 + warp;
+    if (jw >= j1) return;
+    const int nb = L.wp / 32;
+    const int n_cols = (j1 - jw + kWarps - 1) / kWarps;
+    const int total = n_cols * nb;
+    if (total == 0) {
+        for (int j = jw; j < j1; j += kWarps)
+            if (lane == 0) {
+                a.meta[1][linesA + j] = make_uint2(0u, 0u);
+                if (hasB) a.meta[1][linesB + j] = make_uint2(0u, 0u);
+            }
+        return;
+    }
+    size_t po = (size_t)jw * L.wp + lane;
+    int pb = 0;
+    const size_t col_skip = (size_t)(kWarps - 1) * L.wp;
+    auto advance = [&]() {
+        po += 32;
+        if (++pb == nb) {
+            pb = 0;
+            po += col_skip;
+        }
+    };
+    const uint64_t wpol = policy_evict_last();
+    int k0 = ld_w(L.idx + po, wpol);
+    float w0 = ld_w(L.val + po, wpol);
+    advance();
+    int k1 = -1, k2 = -1;
+    float w1 = 0.f, w2 = 0.f;
+    if (total > 1) {
+        k1 = ld_w(L.idx + po, wpol);
+        w1 = ld_w(L.val + po, wpol);
+        advance();
+    }
+    uint2 mA0 = make_uint2(0u, 0u), mB0 = make_uint2(0u, 0u);
+    if (k0 >= 0) {
+        mA0 = imetaA[k0];
+        if (hasB) mB0 = imetaB[k0];
+    }
+    float accA[RPL], accB[RPL];
+    unsigned aliveA = 0u, aliveB = 0u;
+#pragma unroll
+    for (int c = 0; c < RPL; ++c) accA[c] = accB[c] = 0.f;
+    int cj = jw, cb = 0;
+    for (int b = 0; b < total; ++b) {
+        if (b + 2 < total) {
+            k2 = ld_w(L.idx + po, wpol);
+            w2 = ld_w(L.val + po, wpol);
+            advance();
+        }
+        uint2 mA1 = make_uint2(0u, 0u), mB1 = make_uint2(0u, 0u);
+        if (b + 1 < total && k1 >= 0) {
+            mA1 = imetaA[k1];
+            if (hasB) mB1 = imetaB[k1];
+        }
+        const bool la = mA0.x != 0u, lb = mB0.x != 0u;
+        const unsigned live = __ballot_sync(0xffffffffu, la || lb);
+        const int n = __popc(live);
+        const int npad = (n + GB - 1) / GB * GB;
+        {
+            BinEntry2 e;
+            int at;
+            if (la || lb) {
+                e.baseA = la ? mA0.y : 0u;
+                e.baseB = lb ? mB0.y : 0u;
+                e.wA = la ? w0 : 0.f;
+                e.wB = lb ? w0 : 0.f;
+                at = __popc(live & below);
+            } else {
+                e.baseA = e.baseB = 0u;
+                e.wA = e.wB = 0.f;
+                at = n + __popc(~live & below);
+            }
+            if (at < npad) wlist[at] = e;
+        }
+        __syncwarp();
+        auto issue = [&](unsigned (&bA)[GB], unsigned (&bB)[GB], float (&wA)[GB], float (&wB)[GB], int i0) {
+#pragma unroll
+            for (int u = 0; u < GB; ++u) {
+                const BinEntry2 e = wlist[i0 + u];
+                bA[u] = __ldg(inbA + (size_t)e.baseA * 32);
+                bB[u] = __ldg(inbB + (size_t)e.baseB * 32);
+                wA[u] = e.wA;
+                wB[u] = e.wB;
+            }
+        };
+        auto consume = [&](const unsigned (&bA)[GB], const unsigned (&bB)[GB], const float (&wA)[GB],
+                           const float (&wB)[GB]) {
+#pragma unroll
+            for (int u = 0; u < GB; ++u) {
+#pragma unroll
+                for (int c = 0; c < RPL; ++c)
+                    if ((bA[u] >> c) & 1u) accA[c] = __fadd_rn(accA[c], wA[u]);
+#pragma unroll
+                for (int c = 0; c < RPL; ++c)
+                    if ((bB[u] >> c) & 1u) accB[c] = __fadd_rn(accB[c], wB[u]);
+            }
+        };
+        unsigned bA0[GB], bB0[GB], bA1[GB], bB1[GB];
+        float wA0[GB], wB0[GB], wA1[GB], wB1[GB];
+        if (npad) issue(bA0, bB0, wA0, wB0, 0);
+        for (int i0 = 0; i0 < npad; i0 += 2 * GB) {
+            if (i0 + GB < npad) issue(bA1, bB1, wA1, wB1, i0 + GB);
+            consume(bA0, bB0, wA0, wB0);
+            if (i0 + GB >= npad) break;
+            if (i0 + 2 * GB < npad) issue(bA0, bB0, wA0, wB0, i0 + 2 * GB);
+            consume(bA1, bB1, wA1, wB1);
+        }
+        __syncwarp();
+        if (++cb == nb) {
+            cb = 0;
+            auto finish = [&](float (&acc)[RPL], size_t lines, unsigned& alive_bits) {
+                float v[RPL];
+                unsigned bits = 0u;
+#pragma unroll
+                for (int c = 0; c < RPL; ++c) {
+                    bool keep;
+                    v[c] = bias_relu_clamp_keep(acc[c], L.bias, a.ymax, keep);
+                    bits |= keep ? (1u << c) : 0u;
+                    acc[c] = 0.f;
+                }
+                const unsigned om = __ballot_sync(0xffffffffu, bits != 0u);
+                const unsigned hb = (unsigned)cj * 32u;
+                char* out = reinterpret_cast<char*>(a.slab[1]) + lines * kLineBytes;
+                if (bits) st32(out + (size_t)(hb + sector_pos(om, lane)) * 32, v);
+                if (lane == 0) a.meta[1][lines + cj] = make_uint2(om, hb);
+                alive_bits |= bits;
+            };
+            finish(accA, linesA, aliveA);
+            if (hasB) finish(accB, linesB, aliveB);
+            cj += kWarps;
+        }
+        k0 = k1;
+        w0 = w1;
+        mA0 = mA1;
+        mB0 = mB1;
+        k1 = k2;
+        w1 = w2;
+    }
+    if (__any_sync(0xffffffffu, aliveA != 0u))
+        publish_alive<float>(a.alive + ((size_t)1 * a.n_tiles + tA) * AW, aliveA, &a.tile_count[1]);
+    if (hasB && __any_sync(0xffffffffu, aliveB != 0u))
+        publish_alive<float>(a.alive + ((size_t)1 * a.n_tiles + tB) * AW, aliveB, &a.tile_count[1]);
+}
+
 // GB = lines gathered per sub-batch per warp.
 // Shared state of one CTA's walk over a layer.
 template <typename T>
@@ -785,7 +958,7 @@ struct LayerShared {
 // One layer for this CTA: build the ascending live-tile list from the
 // layer's alive flags, then take (tile, output block) items in order from the
 // layer's counter until none are left.
-template <typename T, int GB, bool BIN, bool ZFILL>
+template <typename T, int GB, bool BIN, bool ZFILL, int TP = 1>
 __device__ __forceinline__ void layer_pass(const NetArgs<T>& a, int l, int32_t* tiles, LayerShared<T>& sh) {
     constexpr int AW = alive_words<T>();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -816,7 +989,7 @@ __device__ __forceinline__ void layer_pass(const NetArgs<T>& a, int l, int32_t* 
     const int count = sh.count;
     const LayerDesc<T> L = a.layers[l];
     const int nblk = (a.n_out + a.jb - 1) / a.jb;
-    const long long items = (long long)count * nblk;
+    const long long items = (long long)((count + TP - 1) / TP) * nblk;
     // items are handed out in order from a counter, so all CTAs work on a
     // narrow window of tiles and the tiles' input lines stay in L2 across
     // the 32 columns that gather each of them
@@ -826,29 +999,46 @@ __device__ __forceinline__ void layer_pass(const NetArgs<T>& a, int l, int32_t* 
         const long long it = sh.item;
         __syncthreads();
         if (it >= items) break;
-        const int t = tiles[it / nblk];
+        const int ti = (int)(it / nblk) * TP;
         const int bb = (int)(it % nblk);
         const int j0 = bb * a.jb, j1 = min(a.n_out, j0 + a.jb);
-        layer_item<T, GB, BIN, ZFILL>(a, L, l, t, j0, j1, sh.list[warp]);
+        if constexpr (TP == 2 && BIN && sizeof(T) == 4) {
+            bin_item2<GB>(a, L, tiles[ti], ti + 1 < count ? tiles[ti + 1] : -1, j0, j1,
+                          reinterpret_cast<BinEntry2*>(sh.list[warp]));
+        } else {
+            layer_item<T, GB, BIN, ZFILL>(a, L, l, tiles[ti], j0, j1, sh.list[warp]);
+        }
     }
 }
 
+// Layer-1 (bit-line) tuning, measured on C4: float runs two tiles per item
+// with 2-line sub-batches at 3 CTAs/SM (80 registers); double one tile, 4
+// lines, 4 CTAs/SM.
+#ifndef SDNN_BIN_TP
+#define SDNN_BIN_TP 2
+#endif
 #ifndef SDNN_BIN_GB
-#define SDNN_BIN_GB 4
+#define SDNN_BIN_GB 2
 #endif
 #ifndef SDNN_BIN_OCC
-#define SDNN_BIN_OCC 4
+#define SDNN_BIN_OCC 3
 #endif
-constexpr int kBinGB = SDNN_BIN_GB;  // bit-lines per sub-batch per warp
+template <typename T>
+__host__ __device__ constexpr int bin_gb() { return sizeof(T) == 4 ? SDNN_BIN_GB : 4; }
+template <typename T>
+__host__ __device__ constexpr int bin_occ() { return sizeof(T) == 4 ? SDNN_BIN_OCC : 4; }
 // Layer 1 over binary bit-line tiles, as its own launch so its small
 // register footprint buys more resident warps than the float path's.
 template <typename T>
-__global__ void __launch_bounds__(kThreads, SDNN_BIN_OCC) bin_layer_kernel(NetArgs<T> a) {
+__global__ void __launch_bounds__(kThreads, bin_occ<T>()) bin_layer_kernel(NetArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ LayerShared<T> sh;
     if (a.stamps && blockIdx.x == 0 && threadIdx.x == 0) a.stamps[0] = globaltimer();
     if (__ldcg(&a.tile_count[0]) == 0) return;
-    layer_pass<T, kBinGB, true, false>(a, 0, reinterpret_cast<int32_t*>(smem), sh);
+    if constexpr (sizeof(T) == 4 && SDNN_BIN_TP == 2)
+        layer_pass<T, bin_gb<T>(), true, false, 2>(a, 0, reinterpret_cast<int32_t*>(smem), sh);
+    else
+        layer_pass<T, bin_gb<T>(), true, false>(a, 0, reinterpret_cast<int32_t*>(smem), sh);
 }
 
 // All remaining layers (from a.first_l) in one cooperative launch with a
