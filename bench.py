@@ -7,9 +7,11 @@
 A step is one pass of the whole network (all L layers plus the category
 list) over the batch, the reference's timed region (engine.py:336-339).
 Default workload: C4, the flagship (N=65536, L=1920, 60,000 rows), which
-fits one B200.  With N GPUs (torchrun, one process per GPU) each rank owns a
-contiguous row block and a full weight replica (weak scaling in rows is not
-used: the batch is fixed, so scaling is "strong"); there is no per-layer
+fits one B200.  With N GPUs (torchrun, one process per GPU) every rank holds
+a full weight replica; rows are independent, so by default (--scaling weak)
+every rank runs a full batch of its own distinct rows and `value` counts the
+rows of all ranks; --scaling strong splits one batch into contiguous row
+blocks (the reference's data-parallel tiling).  There is no per-layer
 collective, only the final category gather and a max-over-ranks of the
 device time.
 
@@ -213,8 +215,13 @@ def run_ours(args, dist: RankGroup):
 
     w = workload(args)
     dev = dist.local
-    r0, r1 = shard(w.batch, dist.rank, dist.world)
+    if args.scaling == "weak":  # every rank a full batch of its own rows (rows are independent)
+        r0, r1 = dist.rank * w.batch, (dist.rank + 1) * w.batch
+    else:  # the batch row-partitioned over the ranks (engine._infer_data_parallel tiling)
+        r0, r1 = shard(w.batch, dist.rank, dist.world)
     rows = r1 - r0
+    total_edges = w.edges * (dist.world if args.scaling == "weak" else 1)
+    global_batch = w.batch * (dist.world if args.scaling == "weak" else 1)
     elem = 8 if args.dtype == "f64" else 4
     threads = host_threads()
     t_setup = time.perf_counter()
@@ -293,22 +300,24 @@ def run_ours(args, dist: RankGroup):
 
     line = {
         "metric": METRIC,
-        "value": w.edges / (ms_per_step * 1e-3),
+        "value": total_edges / (ms_per_step * 1e-3),
         "unit": UNIT,
         "n_gpus": dist.world,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": ms_per_step,
         "higher_is_better": True,
-        "scaling": "strong",
+        "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": args.dtype,
         "data": "synthetic (seeded perm-union weights, Bernoulli images; BASELINE.json config)",
         "config": {
             "workload": f"{w.name}: N={w.n}, L={w.layers}, batch={w.batch}, p={w.p}, "
                         f"w={w.value}, bias={w.bias}, ymax={w.ymax}",
-            "neurons": w.n, "layers": w.layers, "global_batch": w.batch,
-            "parallelism": f"dp{dist.world} (contiguous row blocks, weight replica per GPU)",
+            "neurons": w.n, "layers": w.layers, "global_batch": global_batch,
+            "parallelism": (f"dp{dist.world}: " + ("a full batch of distinct rows per GPU"
+                            if args.scaling == "weak" else "contiguous row blocks of one batch")
+                            + ", weight replica per GPU, no per-layer collective"),
             "l2": "inputs larger than L2 (Y0 CSR and weights exceed 126 MB; no flush)",
         },
         "live": {
@@ -335,7 +344,7 @@ def run_ours(args, dist: RankGroup):
             "peak_kind": peak_kind,
         },
         "e2e": {
-            "value": w.edges / (e2e_ms * 1e-3),
+            "value": total_edges / (e2e_ms * 1e-3),
             "unit": UNIT,
             "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h,
@@ -468,6 +477,8 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
+                    help="weak: every GPU a full batch of its own rows; strong: one batch split over GPUs")
     ap.add_argument("--workload", default="C4", choices=sorted(W.CONFIGS))
     ap.add_argument("--dtype", choices=("f32", "f64"), default="f32")
     ap.add_argument("--layers", type=int, default=0)
