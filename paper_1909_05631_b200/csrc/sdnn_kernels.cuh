@@ -1023,10 +1023,13 @@ __device__ __forceinline__ void layer_pass(const NetArgs<T>& a, int l, int32_t* 
 #ifndef SDNN_BIN_OCC
 #define SDNN_BIN_OCC 3
 #endif
+#ifndef SDNN_BIN_OCC64
+#define SDNN_BIN_OCC64 3  // double: 4 CTAs/SM (64 registers) spilled per column
+#endif
 template <typename T>
 __host__ __device__ constexpr int bin_gb() { return sizeof(T) == 4 ? SDNN_BIN_GB : 4; }
 template <typename T>
-__host__ __device__ constexpr int bin_occ() { return sizeof(T) == 4 ? SDNN_BIN_OCC : 4; }
+__host__ __device__ constexpr int bin_occ() { return sizeof(T) == 4 ? SDNN_BIN_OCC : SDNN_BIN_OCC64; }
 // Layer 1 over binary bit-line tiles, as its own launch so its small
 // register footprint buys more resident warps than the float path's.
 template <typename T>
