@@ -41,7 +41,7 @@ def build(force: bool = False, verbose: bool = False) -> None:
     if force or _stale(LIB, deps):
         obj = PKG / "sdnn_gen.o"
         _run(["gcc", "-O3", "-std=gnu11", "-fPIC", "-c", "-o", str(obj), str(gen_src)])
-        cmd = [NVCC, ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-fopenmp",
+        cmd = [NVCC, ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-fopenmp,-mavx2",
                "-cudart", "static", "-o", str(LIB), *map(str, cu), str(obj), "-lpthread", "-lgomp"]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")

@@ -666,15 +666,28 @@ int upload_csr(sdnn_net* net, int64_t n_rows, const int64_t* off, const int64_t*
         char* dst = stage[buf];
         const int cb = b->col_bytes;
         int chunk_bad = 0, chunk_bin = 1;
-#pragma omp parallel for reduction(| : chunk_bad) reduction(& : chunk_bin) schedule(static)
-        for (int64_t p = c0; p < c1; ++p) {
-            const int64_t c = cols[p];
-            chunk_bad |= (c < 0 || c >= n_cols);
-            chunk_bin &= (vals[p] == 1.0);
-            if (cb == 2)
-                reinterpret_cast<uint16_t*>(dst)[p - c0] = (uint16_t)c;
-            else
-                reinterpret_cast<int32_t*>(dst)[p - c0] = (int32_t)c;
+        // branch-free bodies (one loop per column width) so the compiler
+        // vectorises them; this pass is bound by host memory bandwidth
+        const int64_t* cc = cols + c0;
+        const double* vv = vals + c0;
+        const int64_t m = c1 - c0;
+        const uint64_t ncu = (uint64_t)n_cols;
+        if (cb == 2) {
+            uint16_t* d16 = reinterpret_cast<uint16_t*>(dst);
+#pragma omp parallel for simd reduction(| : chunk_bad) reduction(& : chunk_bin) schedule(static)
+            for (int64_t p = 0; p < m; ++p) {
+                chunk_bad |= (int)((uint64_t)cc[p] >= ncu);
+                chunk_bin &= (int)(vv[p] == 1.0);
+                d16[p] = (uint16_t)cc[p];
+            }
+        } else {
+            int32_t* d32 = reinterpret_cast<int32_t*>(dst);
+#pragma omp parallel for simd reduction(| : chunk_bad) reduction(& : chunk_bin) schedule(static)
+            for (int64_t p = 0; p < m; ++p) {
+                chunk_bad |= (int)((uint64_t)cc[p] >= ncu);
+                chunk_bin &= (int)(vv[p] == 1.0);
+                d32[p] = (int32_t)cc[p];
+            }
         }
         bad |= chunk_bad;
         binary &= chunk_bin;
