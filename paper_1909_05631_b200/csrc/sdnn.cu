@@ -494,7 +494,11 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     // its previous (finite) registers and adds them with weight 0, which is
     // exact only when every value the kernel can read is finite.
     const bool zfill = !batch->finite || !std::isfinite((T)ymax) || env_int("SDNN_ZFILL", 0) != 0;
-    const void* fn = zfill ? (const void*)net_kernel<T, 4, true> : (const void*)net_kernel<T, 4, false>;
+#ifndef SDNN_NET_GB
+#define SDNN_NET_GB 4
+#endif
+    const void* fn = zfill ? (const void*)net_kernel<T, SDNN_NET_GB, true>
+                           : (const void*)net_kernel<T, SDNN_NET_GB, false>;
     const size_t smem = (size_t)tiles1 * 4;
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;

@@ -1047,7 +1047,10 @@ __global__ void __launch_bounds__(kThreads, bin_occ<T>()) bin_layer_kernel(NetAr
 // All remaining layers (from a.first_l) in one cooperative launch with a
 // grid barrier between live layers.
 template <typename T, int GB, bool ZFILL>
-__global__ void __launch_bounds__(kThreads, 2 * GB * 8 <= 32 ? 3 : 2)  // y registers
+#ifndef SDNN_NET_OCC
+#define SDNN_NET_OCC 2  // CTAs/SM: the double-buffered 4-line y registers need ~118
+#endif
+__global__ void __launch_bounds__(kThreads, SDNN_NET_OCC)
     net_kernel(NetArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem[];
     int32_t* tiles = reinterpret_cast<int32_t*>(smem);
