@@ -226,7 +226,18 @@ def run_ours(args, dist: RankGroup):
     threads = host_threads()
     t_setup = time.perf_counter()
     net = DeviceNetwork(w.n, dev, args.dtype)
-    net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias, threads=threads)
+    weights = args.weights if args.weights != "auto" else ("broadcast" if dist.world > 1 else "generate")
+    if weights == "broadcast" and dist.world > 1:
+        # rank 0 generates (with every host core), the others receive the
+        # device ELL over NCCL (NVLink/NVSwitch): untimed setup, SURVEY.md 8e
+        if dist.rank == 0:
+            net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias,
+                                     threads=os.cpu_count() or 1)
+        else:
+            net.add_layers_uninit(w.layers, w.width, w.bias)
+        dist.broadcast_layers(net, 0, w.layers)
+    else:
+        net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias, threads=threads)
     off, cols, vals = W.images(w, n_rows=rows, row0=r0, threads=threads)
     nnz0 = int(off[-1])
     batch = net.upload_csr(rows, off, cols, vals)
@@ -477,6 +488,8 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--weights", choices=("auto", "generate", "broadcast"), default="auto",
+                    help="N>1: rank 0 generates, NCCL broadcast to the others (auto), or every rank generates")
     ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
                     help="weak: every GPU a full batch of its own rows; strong: one batch split over GPUs")
     ap.add_argument("--workload", default="C4", choices=sorted(W.CONFIGS))

@@ -79,6 +79,16 @@ int sdnn_net_add_layers_permunion(sdnn_net *net, uint64_t seed, int64_t first_la
                                   int64_t count, int32_t width, double value,
                                   double bias, int threads);
 
+/* Multi-GPU weight replication (weights are replicated once,
+ * untimed, from GPU 0 over NVLink).  sdnn_net_add_layers_uninit appends
+ * `count` layers of ELL width `width` whose device buffers are left for the
+ * caller to fill (e.g. an NCCL broadcast from rank 0); sdnn_net_layer_buffers
+ * exposes a layer's device buffers: idx int32 [n][wp] (-1 = padding) and
+ * val (T) [n][wp], wp = width padded to a multiple of 32. */
+int sdnn_net_add_layers_uninit(sdnn_net *net, int64_t count, int32_t width, double bias);
+int sdnn_net_layer_buffers(const sdnn_net *net, int64_t layer, void **idx, void **val,
+                           int32_t *wp, int64_t *val_bytes);
+
 int sdnn_net_n_layers(const sdnn_net *net, int64_t *n);
 /* Device bytes held by the weights (for the roofline byte model). */
 int sdnn_net_weight_bytes(const sdnn_net *net, int64_t *bytes);

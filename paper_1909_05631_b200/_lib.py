@@ -31,6 +31,8 @@ SIGNATURES = [
     ("sdnn_net_add_layer_csr", cint, [vp, vp, vp, vp, i64, dbl]),
     ("sdnn_net_add_layer_ell", cint, [vp, i32, vp, vp, dbl]),
     ("sdnn_net_add_layers_permunion", cint, [vp, u64, i64, i64, i32, dbl, dbl, cint]),
+    ("sdnn_net_add_layers_uninit", cint, [vp, i64, i32, dbl]),
+    ("sdnn_net_layer_buffers", cint, [vp, i64, P(vp), P(vp), P(i32), P(i64)]),
     ("sdnn_net_n_layers", cint, [vp, P(i64)]),
     ("sdnn_net_weight_bytes", cint, [vp, P(i64)]),
     ("sdnn_batch_upload", cint, [vp, i64, vp, vp, vp, P(vp)]),

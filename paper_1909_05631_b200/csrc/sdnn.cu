@@ -998,6 +998,37 @@ int sdnn_net_add_layers_permunion(sdnn_net* net, uint64_t seed, int64_t first_la
     return SDNN_OK;
 }
 
+int sdnn_net_add_layers_uninit(sdnn_net* net, int64_t count, int32_t width, double bias) {
+    if (!net || count < 0 || width < 0) return fail(SDNN_ERR_PARAMETER, "bad layer request");
+    if (int rc = set_device(net)) return rc;
+    for (int64_t l = 0; l < count; ++l) {
+        DevLayer L;
+        L.width = width;
+        L.wp = (width + 31) / 32 * 32;
+        L.bias = bias;
+        const size_t slots = (size_t)L.wp * (size_t)net->n;
+        CK(cudaMalloc(&L.idx, std::max<size_t>(slots, 1) * sizeof(int32_t)));
+        CK(cudaMalloc(&L.val, std::max<size_t>(slots, 1) * net->elem));
+        L.bytes = (int64_t)slots * (4 + net->elem);
+        net->layers.push_back(L);
+    }
+    return SDNN_OK;
+}
+
+int sdnn_net_layer_buffers(const sdnn_net* net, int64_t layer, void** idx, void** val, int32_t* wp,
+                           int64_t* val_bytes) {
+    if (!net || !idx || !val || !wp || !val_bytes) return fail(SDNN_ERR_PARAMETER, "null argument");
+    if (layer < 0 || layer >= (int64_t)net->layers.size())
+        return fail(SDNN_ERR_PARAMETER, "layer %lld outside the %zu-layer network", (long long)layer,
+                    net->layers.size());
+    const DevLayer& L = net->layers[layer];
+    *idx = L.idx;
+    *val = L.val;
+    *wp = L.wp;
+    *val_bytes = (int64_t)L.wp * net->n * net->elem;
+    return SDNN_OK;
+}
+
 int sdnn_net_n_layers(const sdnn_net* net, int64_t* n) {
     if (!net || !n) return fail(SDNN_ERR_PARAMETER, "null argument");
     *n = (int64_t)net->layers.size();

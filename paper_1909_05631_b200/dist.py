@@ -73,6 +73,19 @@ class RankGroup:
         self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
         return t.cpu().numpy()
 
+    def broadcast_layers(self, net, first: int, count: int) -> None:
+        """Replicate layers [first, first + count) of a DeviceNetwork from
+        rank 0 to every rank, device to device (NCCL over NVLink/NVSwitch):
+        rank 0 generated them, the others appended uninitialised layers of
+        the same shape (DeviceNetwork.add_layers_uninit)."""
+        if self.td is None:
+            return
+        for l in range(first, first + count):
+            idx, val = net.layer_tensors(l)
+            self.td.broadcast(idx, src=0)
+            self.td.broadcast(val, src=0)
+        self.torch.cuda.synchronize(net.device)
+
     def sum(self, x: float) -> float:
         if self.td is None:
             return float(x)

@@ -179,6 +179,14 @@ class DeviceBatch:
             pass
 
 
+class _DevArray:
+    """A device buffer owned by libsdnn, exposed to torch without a copy."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(int(x) for x in shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
 class DeviceNetwork:
     """A network resident on one GPU: every layer converted once to the
     device ELL layout (untimed, like model loading, engine.py:329-332)."""
@@ -226,6 +234,26 @@ class DeviceNetwork:
             self.handle, int(seed), int(first_layer), int(count), int(width), float(value),
             float(bias), int(threads)))
         self.n_layers += int(count)
+
+    def add_layers_uninit(self, count: int, width: int, bias: float) -> None:
+        """Append `count` layers whose device buffers the caller fills (the
+        receiving side of a weight broadcast, dist.broadcast_layers)."""
+        _lib.check(_lib.lib().sdnn_net_add_layers_uninit(self.handle, int(count), int(width), float(bias)))
+        self.n_layers += int(count)
+
+    def layer_tensors(self, layer: int):
+        """(idx, val) torch views of one layer's device buffers, no copy:
+        idx int32 [n, wp] (-1 = padding), val float32/float64 [n, wp]."""
+        import torch
+
+        idx, val = ctypes.c_void_p(), ctypes.c_void_p()
+        wp, vb = ctypes.c_int32(), ctypes.c_int64()
+        _lib.check(_lib.lib().sdnn_net_layer_buffers(self.handle, int(layer), ctypes.byref(idx),
+                                                     ctypes.byref(val), ctypes.byref(wp), ctypes.byref(vb)))
+        vt = "<f8" if self.dtype == "f64" else "<f4"
+        dev = torch.device("cuda", self.device)
+        return (torch.as_tensor(_DevArray(idx.value, (self.n, wp.value), "<i4"), device=dev),
+                torch.as_tensor(_DevArray(val.value, (self.n, wp.value), vt), device=dev))
 
     def set_layer_timing(self, on: bool) -> None:
         _lib.check(_lib.lib().sdnn_net_set_layer_timing(self.handle, 1 if on else 0))

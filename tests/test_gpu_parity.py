@@ -438,3 +438,28 @@ def test_device_weight_ingest_rejects_bad_csr():
     with pytest.raises(ParameterError):
         net.add_layer_csr(bad_off, 0.0)
     net.close()
+
+
+def test_layer_buffers_replicate_a_network():
+    """The weight-replication path of the multi-GPU bench (rank 0 generates,
+    the others receive the device ELL): a network whose layers were filled
+    through the exposed device buffers runs bit-identically to the source."""
+    w, y0, _ = permunion_case(1024, 5, 300, 0.125)
+    for dtype in ("f32", "f64"):
+        src = E.DeviceNetwork(w.n, 0, dtype)
+        src.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias)
+        dst = E.DeviceNetwork(w.n, 0, dtype)
+        dst.add_layers_uninit(w.layers, w.width, w.bias)
+        for l in range(w.layers):
+            si, sv = src.layer_tensors(l)
+            di, dv = dst.layer_tensors(l)
+            assert si.shape == di.shape and sv.dtype == dv.dtype
+            di.copy_(si)
+            dv.copy_(sv)
+        torch.cuda.synchronize()
+        a = src.run(src.upload_csr(y0.n_rows, y0.off, y0.cols, y0.vals), w.ymax, want_y=True)
+        b = dst.run(dst.upload_csr(y0.n_rows, y0.off, y0.cols, y0.vals), w.ymax, want_y=True)
+        assert all(np.array_equal(x, y) for x, y in zip(a.y, b.y))
+        assert np.array_equal(a.categories, b.categories)
+        src.close()
+        dst.close()
