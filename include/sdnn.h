@@ -11,6 +11,7 @@
  *
  *   reference                                   this ABI
  *   engine.infer            engine.py:300-324   sdnn_net_* + sdnn_infer
+ *                                               (sdnn_infer_streamed)
  *   engine.infer_timed      engine.py:327-340   sdnn_batch_upload + sdnn_run
  *                                               (+ sdnn_result_device_ms)
  *   engine._run_layers      engine.py:192-203   sdnn_run (all L layers on device)
@@ -114,6 +115,19 @@ int sdnn_run_y(sdnn_net *net, const sdnn_batch *batch, double ymax, int64_t firs
 /* engine.infer end to end: host CSR in, result (with Y) out. */
 int sdnn_infer(sdnn_net *net, int64_t n_rows, const int64_t *y_off, const int64_t *y_cols,
                const double *y_vals, double ymax, sdnn_result **out);
+
+/* engine.infer end to end with the upload hidden behind the run: Y0 is cut
+ * into `segments` row segments of about equal nnz (0 = automatic: one per
+ * ~96M entries, at most 6); a second host thread converts and uploads
+ * segment s+1 on its own stream while segment s runs.  Rows are independent
+ * (engine.py:237-251), so the result equals the one-shot run bit for bit.
+ * want_y = 0 skips materialising Y (categories only).  sdnn_infer is this
+ * call with want_y = 1 and automatic segments. */
+int sdnn_infer_streamed(sdnn_net *net, int64_t n_rows, const int64_t *y_off, const int64_t *y_cols,
+                        const double *y_vals, double ymax, int want_y, int segments, sdnn_result **out);
+/* Host -> device bytes an end-to-end call copied, and its row segments. */
+int sdnn_result_h2d_bytes(const sdnn_result *r, int64_t *bytes);
+int sdnn_result_segments(const sdnn_result *r, int64_t *n);
 
 /* Category list: 1-based rows of the final Y holding any entry, ascending. */
 int sdnn_result_n_categories(const sdnn_result *r, int64_t *n);

@@ -41,6 +41,9 @@ SIGNATURES = [
     ("sdnn_run", cint, [vp, vp, dbl, i64, i64, P(vp)]),
     ("sdnn_run_y", cint, [vp, vp, dbl, i64, i64, P(vp)]),
     ("sdnn_infer", cint, [vp, i64, vp, vp, vp, dbl, P(vp)]),
+    ("sdnn_infer_streamed", cint, [vp, i64, vp, vp, vp, dbl, cint, cint, P(vp)]),
+    ("sdnn_result_h2d_bytes", cint, [vp, P(i64)]),
+    ("sdnn_result_segments", cint, [vp, P(i64)]),
     ("sdnn_result_n_categories", cint, [vp, P(i64)]),
     ("sdnn_result_categories", cint, [vp, vp]),
     ("sdnn_result_device_ms", dbl, [vp]),

@@ -17,12 +17,16 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <condition_variable>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
 
 #include "../../include/sdnn.h"
 #include "sdnn_kernels.cuh"
+
+#include <omp.h>
 
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
@@ -106,6 +110,7 @@ struct sdnn_net {
     void* descs = nullptr;  // device LayerDesc<T>[layers]
     int64_t descs_n = 0;    // layers mirrored in `descs`
     cudaStream_t stream = nullptr;
+    cudaStream_t ustream = nullptr;  // uploads of a streamed infer (producer thread)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaEvent_t ev_d = nullptr, ev_b = nullptr;  // after densify, after the bit-line layer
     // run scratch, grown on demand
@@ -164,6 +169,8 @@ struct sdnn_result {
     int64_t launches = 0;
     std::vector<double> layer_ms;  // per layer, when layer timing is on
     double stage_ms[3] = {0, 0, 0};  // densify, first (bit-line) layer launch, persistent layer launch
+    int64_t h2d_bytes = 0;  // host -> device bytes of the call's uploads (end-to-end calls)
+    int64_t segments = 0;   // row segments of a streamed call
     bool have_y = false;
     std::vector<int64_t> off, cols;
     std::vector<double> vals;
@@ -637,7 +644,9 @@ int run_impl(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
 // in flight; device buffers come from the stream-ordered pool.
 template <typename T>
 int upload_csr(sdnn_net* net, int64_t n_rows, const int64_t* off, const int64_t* cols,
-               const double* vals, int64_t n_cols, sdnn_batch* b, bool raw = false) {
+               const double* vals, int64_t n_cols, sdnn_batch* b, bool raw = false,
+               cudaStream_t stream = nullptr) {
+    if (!stream) stream = net->stream;
     const int64_t nnz = n_rows > 0 ? off[n_rows] : 0;
     if (n_rows > 0 && off[0] != 0) return fail(SDNN_ERR_PARAMETER, "row_offsets[0] must be 0");
     for (int64_t i = 0; i < n_rows; ++i)
@@ -658,9 +667,9 @@ int upload_csr(sdnn_net* net, int64_t n_rows, const int64_t* off, const int64_t*
             if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     char* stage[2] = {reinterpret_cast<char*>(net->pinned), reinterpret_cast<char*>(net->pinned) + net->pinned_cap};
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&b->off), (n_rows + 1) * sizeof(int64_t), net->stream));
-    CK(cudaMallocAsync(&b->cols, std::max<int64_t>(nnz, 1) * b->col_bytes, net->stream));
-    CK(cudaMemcpyAsync(b->off, off, (n_rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, net->stream));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&b->off), (n_rows + 1) * sizeof(int64_t), stream));
+    CK(cudaMallocAsync(&b->cols, std::max<int64_t>(nnz, 1) * b->col_bytes, stream));
+    CK(cudaMemcpyAsync(b->off, off, (n_rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, stream));
     int bad = 0, binary = 1;
     // pass 1: columns (and the binary check on values)
     int buf = 0;
@@ -696,18 +705,18 @@ int upload_csr(sdnn_net* net, int64_t n_rows, const int64_t* off, const int64_t*
         bad |= chunk_bad;
         binary &= chunk_bin;
         CK(cudaMemcpyAsync(reinterpret_cast<char*>(b->cols) + c0 * cb, dst, (c1 - c0) * cb, cudaMemcpyHostToDevice,
-                           net->stream));
-        CK(cudaEventRecord(net->stage_ev[buf], net->stream));
+                           stream));
+        CK(cudaEventRecord(net->stage_ev[buf], stream));
     }
     if (bad) {
-        CK(cudaStreamSynchronize(net->stream));
+        CK(cudaStreamSynchronize(stream));
         return fail(SDNN_ERR_PARAMETER, "column index outside [0, %lld)", (long long)n_cols);
     }
     b->h2d_bytes += nnz * b->col_bytes;
     b->vals = nullptr;
     if (raw || env_int("SDNN_FORCE_VALUES", 0)) binary = 0;
     if (!binary) {  // pass 2: values
-        CK(cudaMallocAsync(&b->vals, std::max<int64_t>(nnz, 1) * sizeof(T), net->stream));
+        CK(cudaMallocAsync(&b->vals, std::max<int64_t>(nnz, 1) * sizeof(T), stream));
         for (int64_t c0 = 0; c0 < nnz; c0 += chunk, buf ^= 1) {
             const int64_t c1 = std::min(nnz, c0 + chunk);
             CK(cudaEventSynchronize(net->stage_ev[buf]));
@@ -720,12 +729,12 @@ int upload_csr(sdnn_net* net, int64_t n_rows, const int64_t* off, const int64_t*
             }
             b->finite = b->finite && chunk_fin;
             CK(cudaMemcpyAsync(reinterpret_cast<T*>(b->vals) + c0, dst, (c1 - c0) * sizeof(T), cudaMemcpyHostToDevice,
-                               net->stream));
-            CK(cudaEventRecord(net->stage_ev[buf], net->stream));
+                               stream));
+            CK(cudaEventRecord(net->stage_ev[buf], stream));
         }
         b->h2d_bytes += nnz * (int64_t)sizeof(T);
     }
-    CK(cudaStreamSynchronize(net->stream));
+    CK(cudaStreamSynchronize(stream));
     return SDNN_OK;
 }
 
@@ -893,6 +902,153 @@ int make_net(int device, int dtype, int64_t n, sdnn_net** out) {
     return SDNN_OK;
 }
 
+
+// engine.infer end to end with the upload hidden behind the run.  Y0 is cut
+// into row segments of about equal nnz; a producer thread converts and
+// uploads segment s+1 (host memory bound: int64/float64 CSR in) on its own
+// stream while segment s runs on the engine stream.  Rows are independent
+// (engine.py:237-251 tiles them the same way), so the segments' outputs
+// concatenate to exactly the one-shot result.
+int auto_segments(int64_t n_rows, int64_t nnz) {
+    const int64_t forced = env_int("SDNN_SEGMENTS", 0);
+    if (forced > 0) return (int)std::min<int64_t>(forced, std::max<int64_t>(n_rows, 1));
+    const int64_t per = 96ll << 20;  // entries per segment: ~1 GB of host CSR
+    int64_t s = std::min<int64_t>(nnz / per, 6);
+    s = std::min<int64_t>(s, n_rows / 4096);
+    return (int)std::max<int64_t>(s, 1);
+}
+
+void merge_part(sdnn_result* res, const sdnn_result& part, int64_t r0, int want_y) {
+    for (int64_t c : part.cats) res->cats.push_back(c + r0);
+    for (size_t l = 0; l < part.live.size(); ++l) res->live[l] += part.live[l];
+    res->dev_ms += part.dev_ms;
+    res->launches += part.launches;
+    for (int k = 0; k < 3; ++k) res->stage_ms[k] += part.stage_ms[k];
+    for (size_t l = 0; l < part.layer_ms.size() && l < res->layer_ms.size(); ++l) res->layer_ms[l] += part.layer_ms[l];
+    if (want_y) {
+        const int64_t base = res->off[r0];
+        for (int64_t r = 1; r < (int64_t)part.off.size(); ++r) res->off[r0 + r] = base + part.off[r];
+        res->cols.insert(res->cols.end(), part.cols.begin(), part.cols.end());
+        res->vals.insert(res->vals.end(), part.vals.begin(), part.vals.end());
+    }
+}
+
+template <typename T>
+int infer_streamed(sdnn_net* net, int64_t n_rows, const int64_t* off, const int64_t* cols, const double* vals,
+                   double ymax, int want_y, int segments, sdnn_result* res) {
+    const int64_t L = (int64_t)net->layers.size();
+    if (L < 1) return fail(SDNN_ERR_PARAMETER, "the network has no layers");
+    if (n_rows > 0 && off[0] != 0) return fail(SDNN_ERR_PARAMETER, "row_offsets[0] must be 0");
+    for (int64_t i = 0; i < n_rows; ++i)
+        if (off[i + 1] < off[i]) return fail(SDNN_ERR_PARAMETER, "row_offsets non-monotone at %lld", (long long)i);
+    const int64_t nnz = n_rows > 0 ? off[n_rows] : 0;
+    const int S = segments > 0 ? (int)std::min<int64_t>(segments, std::max<int64_t>(n_rows, 1))
+                               : auto_segments(n_rows, nnz);
+    if (int rc = sync_descs<T>(net)) return rc;
+    struct Seg {
+        int64_t r0 = 0, r1 = 0;
+        std::vector<int64_t> off;
+        sdnn_batch* b = nullptr;
+        int rc = 0;
+        std::string err;
+    };
+    std::vector<Seg> seg(S);
+    for (int s = 0; s < S; ++s) {  // row bounds at equal shares of the entries
+        auto at = [&](int k) -> int64_t {
+            if (k == 0) return 0;
+            if (k == S) return n_rows;
+            if (nnz == 0) return n_rows * k / S;
+            const int64_t want = nnz * k / S;
+            return std::min<int64_t>(std::lower_bound(off, off + n_rows + 1, want) - off, n_rows);
+        };
+        seg[s].r0 = at(s);
+        seg[s].r1 = std::max(at(s + 1), seg[s].r0);
+    }
+    res->n_rows = n_rows;
+    res->n_cols = net->n;
+    res->n_layers = L;
+    res->live.assign(L + 1, 0);
+    res->segments = S;
+    if (net->layer_timing) res->layer_ms.assign(L, 0.0);
+    if (want_y) res->off.assign(n_rows + 1, 0);
+    if (!net->ustream) CK(cudaStreamCreateWithFlags(&net->ustream, cudaStreamNonBlocking));
+
+    std::mutex mu;
+    std::condition_variable cv;
+    int ready = 0;  // segments whose upload finished (or failed)
+    bool stop = false;
+    const int threads = host_threads();
+    std::thread producer([&] {
+        cudaSetDevice(net->device);
+        omp_set_num_threads(std::max(1, threads - 1));  // one core runs the engine stream
+        for (int s = 0; s < S; ++s) {
+            {
+                std::lock_guard<std::mutex> g(mu);
+                if (stop) break;
+            }
+            Seg& g = seg[s];
+            const int64_t rows = g.r1 - g.r0, c0 = off[g.r0];
+            g.off.resize(rows + 1);
+            for (int64_t i = 0; i <= rows; ++i) g.off[i] = off[g.r0 + i] - c0;
+            g.b = new sdnn_batch;
+            g.b->net = net;
+            g.rc = upload_csr<T>(net, rows, g.off.data(), cols ? cols + c0 : cols, vals ? vals + c0 : vals, net->n,
+                                 g.b, false, net->ustream);
+            if (g.rc) g.err = g_err;
+            {
+                std::lock_guard<std::mutex> lk(mu);
+                ready = s + 1;
+                if (g.rc) stop = true;
+            }
+            cv.notify_one();
+            if (g.rc) break;
+        }
+        std::lock_guard<std::mutex> lk(mu);
+        stop = true;
+        cv.notify_one();
+    });
+    int rc = SDNN_OK;
+    for (int s = 0; s < S && rc == SDNN_OK; ++s) {
+        {
+            std::unique_lock<std::mutex> lk(mu);
+            cv.wait(lk, [&] { return ready > s || stop; });
+            if (ready <= s) {  // the producer stopped before this segment
+                rc = -1;
+                break;
+            }
+        }
+        Seg& g = seg[s];
+        if (g.rc) {
+            rc = g.rc;
+            g_err = g.err;
+            break;
+        }
+        sdnn_result part;
+        rc = run_impl<T>(net, g.b, ymax, 0, L, want_y, 1, net->n, net->n, &part);
+        if (rc == SDNN_OK) {
+            merge_part(res, part, g.r0, want_y);
+            res->h2d_bytes += g.b->h2d_bytes;
+        }
+    }
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        stop = true;
+    }
+    producer.join();
+    for (auto& g : seg)
+        if (g.b) free_batch(g.b);
+    if (rc < 0) {  // a segment failed after an earlier one: report its error
+        for (auto& g : seg)
+            if (g.rc) {
+                g_err = g.err;
+                return g.rc;
+            }
+        return fail(SDNN_ERR_CAPACITY, "streamed upload stopped early");
+    }
+    if (rc == SDNN_OK && want_y) res->have_y = true;
+    return rc;
+}
+
 }  // namespace
 
 // ===================================================================== C ABI
@@ -953,6 +1109,7 @@ void sdnn_net_destroy(sdnn_net* net) {
     if (net->ev_d) cudaEventDestroy(net->ev_d);
     if (net->ev_b) cudaEventDestroy(net->ev_b);
     if (net->stream) cudaStreamDestroy(net->stream);
+    if (net->ustream) cudaStreamDestroy(net->ustream);
     delete net;
 }
 
@@ -1106,15 +1263,43 @@ int sdnn_run_y(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t firs
     return run_checked(net, batch, ymax, first_layer, n_layers, 1, out);
 }
 
+int sdnn_infer_streamed(sdnn_net* net, int64_t n_rows, const int64_t* y_off, const int64_t* y_cols,
+                        const double* y_vals, double ymax, int want_y, int segments, sdnn_result** out) {
+    if (!net || !out || n_rows < 0 || (n_rows > 0 && !y_off)) return fail(SDNN_ERR_PARAMETER, "bad batch");
+    if (n_rows >= (1LL << 31)) return fail(SDNN_ERR_CAPACITY, "batch of %lld rows exceeds int32 row ids", (long long)n_rows);
+    if (!(ymax > 0)) return fail(SDNN_ERR_PARAMETER, "ymax must be positive, got %g", ymax);
+    if (int rc = set_device(net)) return rc;
+    static const int64_t zero_off[1] = {0};
+    const int64_t* off = n_rows > 0 ? y_off : zero_off;
+    const double t0 = now_ms();
+    sdnn_result* res = new sdnn_result;
+    int rc = net->dtype == SDNN_F64
+                 ? infer_streamed<double>(net, n_rows, off, y_cols, y_vals, ymax, want_y, segments, res)
+                 : infer_streamed<float>(net, n_rows, off, y_cols, y_vals, ymax, want_y, segments, res);
+    if (rc) {
+        delete res;
+        return rc;
+    }
+    res->wall_ms = now_ms() - t0;
+    *out = res;
+    return SDNN_OK;
+}
+
 int sdnn_infer(sdnn_net* net, int64_t n_rows, const int64_t* y_off, const int64_t* y_cols,
                const double* y_vals, double ymax, sdnn_result** out) {
-    const double t0 = now_ms();
-    sdnn_batch* b = nullptr;
-    if (int rc = sdnn_batch_upload(net, n_rows, y_off, y_cols, y_vals, &b)) return rc;
-    int rc = run_checked(net, b, ymax, 0, -1, 1, out);
-    sdnn_batch_free(b);
-    if (rc == SDNN_OK) (*out)->wall_ms = now_ms() - t0;
-    return rc;
+    return sdnn_infer_streamed(net, n_rows, y_off, y_cols, y_vals, ymax, 1, 0, out);
+}
+
+int sdnn_result_h2d_bytes(const sdnn_result* r, int64_t* bytes) {
+    if (!r || !bytes) return fail(SDNN_ERR_PARAMETER, "null argument");
+    *bytes = r->h2d_bytes;
+    return SDNN_OK;
+}
+
+int sdnn_result_segments(const sdnn_result* r, int64_t* n) {
+    if (!r || !n) return fail(SDNN_ERR_PARAMETER, "null argument");
+    *n = r->segments;
+    return SDNN_OK;
 }
 
 int sdnn_result_n_categories(const sdnn_result* r, int64_t* n) {

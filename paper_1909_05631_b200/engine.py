@@ -150,6 +150,8 @@ class RunResult:
     y: tuple | None = None      # (off, cols, vals) float64 CSR, when requested
     layer_ms: np.ndarray | None = None  # per layer, when layer timing is on
     stage_ms: np.ndarray | None = None  # [densify, bit-line layer launch, persistent launch]
+    h2d_bytes: int = 0          # end-to-end calls: host -> device bytes copied
+    segments: int = 0           # end-to-end calls: row segments streamed
 
 
 class DeviceBatch:
@@ -285,18 +287,32 @@ class DeviceNetwork:
         finally:
             L.sdnn_result_free(h)
 
-    def infer_host(self, y0, ymax: float = DEFAULT_YMAX) -> RunResult:
-        """End-to-end C-ABI call (sdnn_infer): host CSR in, categories + Y out."""
+    def infer_host(self, y0, ymax: float = DEFAULT_YMAX, want_y: bool = True,
+                   segments: int = 0) -> RunResult:
+        """End-to-end C-ABI call (sdnn_infer_streamed): host CSR in,
+        categories (+ Y) out; the upload of row segment s+1 overlaps the run
+        of segment s."""
         n_rows, n_cols, off, cols, vals = _csr(y0)
         if n_cols != self.n:
             raise ShapeError(f"input has {n_cols} columns but the model expects {self.n} neurons")
+        return self.infer_csr(n_rows, off, cols, vals, ymax, want_y, segments)
+
+    def infer_csr(self, n_rows, off, cols, vals, ymax: float = DEFAULT_YMAX, want_y: bool = True,
+                  segments: int = 0) -> RunResult:
         L = _lib.lib()
         h = ctypes.c_void_p()
-        _lib.check(L.sdnn_infer(self.handle, n_rows, _lib.ptr(_nonempty(off, np.int64)),
-                                _lib.ptr(_nonempty(cols, np.int64)),
-                                _lib.ptr(_nonempty(vals, np.float64)), float(ymax), ctypes.byref(h)))
+        _lib.check(L.sdnn_infer_streamed(
+            self.handle, int(n_rows), _lib.ptr(_nonempty(np.ascontiguousarray(off, np.int64), np.int64)),
+            _lib.ptr(_nonempty(np.ascontiguousarray(cols, np.int64), np.int64)),
+            _lib.ptr(_nonempty(np.ascontiguousarray(vals, np.float64), np.float64)), float(ymax),
+            1 if want_y else 0, int(segments), ctypes.byref(h)))
         try:
-            return _collect(h, n_rows, True)
+            r = _collect(h, int(n_rows), want_y)
+            b, s = ctypes.c_int64(), ctypes.c_int64()
+            _lib.check(L.sdnn_result_h2d_bytes(h, ctypes.byref(b)))
+            _lib.check(L.sdnn_result_segments(h, ctypes.byref(s)))
+            r.h2d_bytes, r.segments = b.value, s.value
+            return r
         finally:
             L.sdnn_result_free(h)
 
@@ -394,6 +410,8 @@ def _run_block(model, dtype, device, ymax, n_rows, off, cols, vals, ranges):
     """Push one row block through the given layer ranges on one GPU."""
     net = _device_network(model, device, dtype)
     with net.lock:
+        if ranges == [(0, model.n_layers)]:  # one range: upload streamed behind the run
+            return net.infer_csr(n_rows, off, cols, vals, ymax, want_y=True).y
         for lo, hi in ranges:
             batch = net.upload_csr(n_rows, off, cols, vals)
             try:

@@ -245,6 +245,59 @@ def test_e2e_host_call_matches_device_resident_run():
     assert all(np.array_equal(x, y) for x, y in zip(a.y, b.y))
 
 
+@pytest.mark.parametrize("segments", [1, 2, 3, 7, 1000])
+@pytest.mark.parametrize("dtype,prec", [("f64", 64), ("f32", 32)])
+def test_streamed_e2e_segments_are_bit_identical(segments, dtype, prec):
+    """sdnn_infer_streamed: Y0 uploaded in row segments by a second host
+    thread while earlier segments run; every segment count gives the
+    oracle's result bit for bit.  One segment holds real values (float
+    tiles), the others are binary (bit-line tiles), and a block of empty
+    rows sits in the middle."""
+    w, y0, layers = permunion_case(1024, 6, 300, 0.125)
+    vals = y0.vals.copy()
+    lo, hi = int(y0.off[200]), int(y0.off[260])
+    vals[lo:hi] = 0.75
+    off = y0.off.copy()
+    cols = y0.cols.copy()
+    # rows 100..139 empty
+    keep = np.ones(cols.size, bool)
+    keep[int(off[100]):int(off[140])] = False
+    counts = np.diff(off)
+    counts[100:140] = 0
+    off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    cols, vals = cols[keep], vals[keep]
+    yy = O.CSR(y0.n_rows, w.n, off, cols, vals)
+    net = E.DeviceNetwork(w.n, 0, dtype)
+    net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias)
+    got = net.infer_csr(yy.n_rows, off, cols, vals, w.ymax, want_y=True, segments=segments)
+    assert got.segments == min(segments, yy.n_rows)
+    want = O.infer(layers, [w.bias] * w.layers, yy, precision=prec, threads=8)
+    assert O.CSR(yy.n_rows, w.n, *got.y).identical(want)
+    assert np.array_equal(got.categories, O.categorize(want))
+    ref = net.run(net.upload_csr(yy.n_rows, off, cols, vals), w.ymax)
+    assert np.array_equal(got.live_rows, ref.live_rows)
+    cats_only = net.infer_csr(yy.n_rows, off, cols, vals, w.ymax, want_y=False, segments=segments)
+    assert cats_only.y is None and np.array_equal(cats_only.categories, got.categories)
+    assert cats_only.h2d_bytes > 0
+    net.close()
+
+
+def test_streamed_e2e_empty_batch_and_bad_input():
+    w, y0, layers = permunion_case(1024, 2, 10, 0.125)
+    net = E.DeviceNetwork(w.n, 0, "f32")
+    net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias)
+    r = net.infer_csr(0, np.zeros(1, np.int64), np.zeros(0, np.int64), np.zeros(0), w.ymax)
+    assert r.categories.size == 0 and r.y[0].tolist() == [0]
+    bad = y0.cols.copy()
+    bad[-1] = w.n  # column outside the row: ParameterError from the producer thread
+    with pytest.raises(ParameterError):
+        net.infer_csr(y0.n_rows, y0.off, bad, y0.vals, w.ymax, segments=3)
+    # the handle stays usable after the failed call
+    ok = net.infer_csr(y0.n_rows, y0.off, y0.cols, y0.vals, w.ymax, segments=3)
+    assert np.array_equal(ok.categories, O.categorize(O.infer(layers, [w.bias] * 2, y0, precision=32)))
+    net.close()
+
+
 # ------------------------------------------------ BASELINE configs, full size
 
 def test_c1_as_specified_full_size():

@@ -1,8 +1,9 @@
 #!/bin/bash
-# e2e upload/run split for several builds: LIBS="a.so b.so"
-for v in ${LIBS:-""}; do
-  SDNN_LIB=$v timeout 900 python bench.py --steps 5 --warmup 2 --companions '' --no-cpu 2>/dev/null | tail -1 | python -c "
+# e2e (streamed C-ABI call) for several segment counts: SEGS="1 2 4 6"
+for s in ${SEGS:-"0"}; do
+  SDNN_SEGMENTS=$s timeout 900 python bench.py --steps 5 --warmup 3 --companions '' --no-cpu 2>/dev/null | tail -1 | python -c "
 import json,sys
 d=json.loads(sys.stdin.read())
-print('$v', 'e2e ms %.1f'%d['e2e']['ms_per_step'], d['e2e']['upload_run_ms_per_step'])"
+e=d['e2e']
+print('segments $s', 'ms/step %.2f'%d['ms_per_step'], 'e2e ms %.1f'%e['ms_per_step'], 'segs', e['segments'], 'split', e['unstreamed_upload_then_run_ms'])"
 done
