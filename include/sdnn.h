@@ -20,6 +20,7 @@
  *   challenge.categorize    challenge.py:60-67  sdnn_result_categories
  *   NetworkModel/LayerWeights model.py:128-162  sdnn_net_add_layer_csr
  *   FeatureBatch result     engine.py:158-160,324  sdnn_result_y_csr
+ *   ingest.resize_threshold_flatten ingest.py:128-156  sdnn_batch_from_images
  *
  * Return codes map onto the reference's exception classes
  * (errors.py:12,46,50):  0 ok, 2 ParameterError, 3 CapacityError (also any
@@ -97,7 +98,22 @@ int sdnn_net_weight_bytes(const sdnn_net *net, int64_t *bytes);
 /* Stage Y0 (FeatureBatch, CSR) on the device.  Untimed input placement. */
 int sdnn_batch_upload(sdnn_net *net, int64_t n_rows, const int64_t *y_off,
                       const int64_t *y_cols, const double *y_vals, sdnn_batch **out);
+/* A batch lives in its network's stream and memory pool: free it before
+ * sdnn_net_destroy of that network. */
 void sdnn_batch_free(sdnn_batch *batch);
+/* ingest.resize_threshold_flatten (ingest.py:128-156) on the device: n_images
+ * square uint8 images of side x side pixels (ImageSet.pixels, row-major)
+ * -> pixels / 255, bilinear resample to target_side (32, 64, 128 or 256, the
+ * reference's TARGET_SIDES; ParameterError otherwise), threshold >= 0.5,
+ * flatten row-major: a binary batch staged on the device, bit-identical to
+ * the reference's FeatureBatch.  ShapeError unless target_side^2 equals the
+ * network's neuron count. */
+int sdnn_batch_from_images(sdnn_net *net, int64_t n_images, int32_t side, const uint8_t *pixels,
+                           int32_t target_side, sdnn_batch **out);
+/* A staged batch back as host CSR (values 1.0 for a binary batch; cols and
+ * vals may be null): query nnz first. */
+int sdnn_batch_nnz(const sdnn_batch *batch, int64_t *nnz);
+int sdnn_batch_csr(const sdnn_batch *batch, int64_t *off, int64_t *cols, double *vals);
 /* Bytes the upload copied host -> device (offsets, columns as uint16 when
  * the row length is <= 65536 else int32, values unless all are 1.0). */
 int sdnn_batch_h2d_bytes(const sdnn_batch *batch, int64_t *bytes);

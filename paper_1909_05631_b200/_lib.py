@@ -37,6 +37,9 @@ SIGNATURES = [
     ("sdnn_net_weight_bytes", cint, [vp, P(i64)]),
     ("sdnn_batch_upload", cint, [vp, i64, vp, vp, vp, P(vp)]),
     ("sdnn_batch_free", None, [vp]),
+    ("sdnn_batch_from_images", cint, [vp, i64, i32, vp, i32, P(vp)]),
+    ("sdnn_batch_nnz", cint, [vp, P(i64)]),
+    ("sdnn_batch_csr", cint, [vp, vp, vp, vp]),
     ("sdnn_batch_h2d_bytes", cint, [vp, P(i64)]),
     ("sdnn_run", cint, [vp, vp, dbl, i64, i64, P(vp)]),
     ("sdnn_run_y", cint, [vp, vp, dbl, i64, i64, P(vp)]),

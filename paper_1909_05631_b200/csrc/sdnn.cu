@@ -174,6 +174,21 @@ struct sdnn_result {
     bool have_y = false;
     std::vector<int64_t> off, cols;
     std::vector<double> vals;
+    // Y kept on the device (single-wave runs): canonical CSR, copied straight
+    // into the caller's buffers by sdnn_result_y_csr
+    int device = -1;
+    int64_t* d_off = nullptr;
+    int64_t* d_cols = nullptr;
+    double* d_vals = nullptr;
+    int64_t d_nnz = 0;
+    ~sdnn_result() {
+        if (d_off || d_cols || d_vals) {
+            cudaSetDevice(device);
+            cudaFree(d_off);
+            cudaFree(d_cols);
+            cudaFree(d_vals);
+        }
+    }
 };
 
 namespace {
@@ -412,6 +427,143 @@ __global__ void live_rows_kernel(const uint32_t* __restrict__ alive, int n_tiles
     }
 }
 
+// Final Y of a single-wave run, materialised on the device in the
+// reference's layout (engine._wrap, engine.py:158-160: row-ordered canonical
+// CSR, int64 columns, float64 values); sdnn_result_y_csr then copies it
+// straight into the caller's buffers.  Returns 1 (nothing allocated) when
+// the device cannot hold it, so the caller falls back to host assembly.
+template <typename T>
+int extract_device(sdnn_net* net, const T* slab, const uint2* meta, int ld, int n_cols, int64_t n_tiles,
+                   const uint32_t* alive_last, int64_t B, sdnn_result* res) {
+    constexpr int TR = tile_rows<T>();
+    const int64_t lanes = n_tiles * TR;
+    cudaStream_t st = net->stream;
+    int32_t* counts = nullptr;
+    int64_t* rowcnt = nullptr;
+    auto give_up = [&]() {
+        cudaGetLastError();  // clear the allocation failure
+        if (counts) cudaFree(counts);
+        if (rowcnt) cudaFree(rowcnt);
+        cudaFree(res->d_off);
+        cudaFree(res->d_cols);
+        cudaFree(res->d_vals);
+        res->d_off = res->d_cols = nullptr;
+        res->d_vals = nullptr;
+        return 1;
+    };
+    res->device = net->device;
+    if (cudaMalloc(&res->d_off, (B + 1) * 8) != cudaSuccess) return give_up();
+    if (cudaMalloc(&rowcnt, (B + 1) * 8) != cudaSuccess) return give_up();
+    if (lanes && cudaMalloc(&counts, lanes * 4) != cudaSuccess) return give_up();
+    CK(cudaMemsetAsync(rowcnt, 0, (B + 1) * 8, st));
+    if (lanes) {
+        const int grid = (int)std::min<int64_t>((n_tiles + 7) / 8, (int64_t)net->sm_count * 16);
+        extract_kernel<T><<<grid, 256, 0, st>>>(slab, meta, ld, n_cols, (int)n_tiles, nullptr, counts, nullptr,
+                                                nullptr);
+        CK(cudaGetLastError());
+        row_counts_kernel<T><<<(unsigned)std::min<int64_t>((lanes + 255) / 256, 4096), 256, 0, st>>>(
+            counts, net->rowid, alive_last, lanes, rowcnt);
+        CK(cudaGetLastError());
+    }
+    size_t tmp_bytes = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, rowcnt, res->d_off, (int)(B + 1), st));
+    if (tmp_bytes > net->cub_cap) {
+        if (net->cub_tmp) CK(cudaFree(net->cub_tmp));
+        CK(cudaMalloc(&net->cub_tmp, tmp_bytes));
+        net->cub_cap = tmp_bytes;
+    }
+    CK(cub::DeviceScan::ExclusiveSum(net->cub_tmp, tmp_bytes, rowcnt, res->d_off, (int)(B + 1), st));
+    int64_t nnz = 0;
+    CK(cudaMemcpyAsync(&nnz, res->d_off + B, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (cudaMalloc(&res->d_cols, std::max<int64_t>(nnz, 1) * 8) != cudaSuccess) return give_up();
+    if (cudaMalloc(&res->d_vals, std::max<int64_t>(nnz, 1) * 8) != cudaSuccess) return give_up();
+    if (nnz) {
+        const int grid = (int)std::min<int64_t>((n_tiles + 7) / 8, (int64_t)net->sm_count * 16);
+        extract_rows_kernel<T><<<grid, 256, 0, st>>>(slab, meta, ld, n_cols, (int)n_tiles, alive_last, net->rowid,
+                                                     res->d_off, res->d_cols, res->d_vals);
+        CK(cudaGetLastError());
+    }
+    CK(cudaStreamSynchronize(st));
+    cudaFree(counts);
+    cudaFree(rowcnt);
+    res->d_nnz = nnz;
+    res->have_y = true;
+    return SDNN_OK;
+}
+
+// Large device -> pageable host copy: chunks go through two pinned staging
+// buffers (DMA at full link speed) while host threads copy the previous
+// chunk out in parallel (which also spreads the first-touch page faults of
+// a freshly allocated destination over all cores).
+int d2h_large(void* dst, const void* src, size_t bytes) {
+    constexpr size_t kChunk = 64ull << 20;
+    if (bytes <= kChunk) {
+        CK(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+        return SDNN_OK;
+    }
+    char* stage = nullptr;
+    CK(cudaMallocHost(&stage, 2 * kChunk));
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    int rc = SDNN_OK;
+    auto check = [&](cudaError_t e) {
+        if (e != cudaSuccess && rc == SDNN_OK)
+            rc = fail(SDNN_ERR_CAPACITY, "Y copy failed: %s", cudaGetErrorString(e));
+        return e == cudaSuccess;
+    };
+    if (check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) && check(cudaEventCreate(&ev[0])) &&
+        check(cudaEventCreate(&ev[1]))) {
+        const size_t n = (bytes + kChunk - 1) / kChunk;
+        for (size_t i = 0; i <= n && rc == SDNN_OK; ++i) {
+            if (i < n) {  // chunk i -> buffer i & 1
+                const size_t len = std::min(kChunk, bytes - i * kChunk);
+                check(cudaMemcpyAsync(stage + (i & 1) * kChunk, static_cast<const char*>(src) + i * kChunk, len,
+                                      cudaMemcpyDeviceToHost, st));
+                check(cudaEventRecord(ev[i & 1], st));
+            }
+            if (i > 0) {  // chunk i-1 out of its buffer, in parallel
+                const size_t j = i - 1, len = std::min(kChunk, bytes - j * kChunk);
+                if (!check(cudaEventSynchronize(ev[j & 1]))) break;
+                const char* from = stage + (j & 1) * kChunk;
+                char* to = static_cast<char*>(dst) + j * kChunk;
+                const int64_t parts = 64;
+#pragma omp parallel for schedule(static)
+                for (int64_t q = 0; q < parts; ++q) {
+                    const size_t a = len * q / parts, b = len * (q + 1) / parts;
+                    memcpy(to + a, from + a, b - a);
+                }
+            }
+        }
+    }
+    if (st) cudaStreamSynchronize(st);
+    for (auto e : ev)
+        if (e) cudaEventDestroy(e);
+    if (st) cudaStreamDestroy(st);
+    cudaFreeHost(stage);
+    return rc;
+}
+
+// Device-held Y -> the result's host vectors (for merging streamed parts).
+int y_to_host(sdnn_result* r) {
+    if (!r->d_off) return SDNN_OK;
+    CK(cudaSetDevice(r->device));
+    r->off.resize(r->n_rows + 1);
+    r->cols.resize(r->d_nnz);
+    r->vals.resize(r->d_nnz);
+    if (int rc = d2h_large(r->off.data(), r->d_off, (r->n_rows + 1) * 8)) return rc;
+    if (r->d_nnz) {
+        if (int rc = d2h_large(r->cols.data(), r->d_cols, r->d_nnz * 8)) return rc;
+        if (int rc = d2h_large(r->vals.data(), r->d_vals, r->d_nnz * 8)) return rc;
+    }
+    cudaFree(r->d_off);
+    cudaFree(r->d_cols);
+    cudaFree(r->d_vals);
+    r->d_off = r->d_cols = nullptr;
+    r->d_vals = nullptr;
+    return SDNN_OK;
+}
+
 // One wave of rows [r0, r1) through layers [first, first + nl).
 template <typename T>
 int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first, int64_t nl, int epilogue,
@@ -593,6 +745,15 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     for (int64_t t = 0; t < n_tiles; ++t)
         for (int r = 0; r < TR; ++r)
             if ((alive_last[t * AW + r / 32] >> (r % 32)) & 1u) final_rows.push_back(rowid[t * TR + r]);
+    if (want_y && r0 == 0 && r1 == batch->n_rows && env_int("SDNN_HOST_Y", 0) == 0) {
+        // the whole batch in one wave: Y goes straight into a device CSR
+        const int last = (int)(nl & 1);
+        res->n_rows = batch->n_rows;
+        int rc = extract_device<T>(net, reinterpret_cast<const T*>(net->slab[last]), net->meta[last], (int)ld,
+                                   (int)n_out, n_tiles, net->alive + nl * tiles1 * AW, batch->n_rows, res);
+        if (rc == SDNN_OK) return SDNN_OK;
+        if (rc != 1) return rc;  // a CUDA failure; 1 = no room, assemble on the host instead
+    }
     if (want_y) {
         Piece p;
         const int last = (int)(nl & 1);  // layer nl-1 wrote buffer nl & 1
@@ -631,7 +792,7 @@ int run_impl(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     res->cats.resize(final_rows.size());
     for (size_t i = 0; i < final_rows.size(); ++i) res->cats[i] = (int64_t)final_rows[i] + 1;
     res->dev_ms = dev_ms;
-    if (want_y) assemble(res, pieces);
+    if (want_y && !res->d_off) assemble(res, pieces);
     return SDNN_OK;
 }
 
@@ -735,6 +896,105 @@ int upload_csr(sdnn_net* net, int64_t n_rows, const int64_t* off, const int64_t*
         b->h2d_bytes += nnz * (int64_t)sizeof(T);
     }
     CK(cudaStreamSynchronize(stream));
+    return SDNN_OK;
+}
+
+// ingest.resize_threshold_flatten (ingest.py:128-156) on the device: raw
+// uint8 images in, the binary feature batch (device CSR, no values) out.
+// The interpolation taps are computed here exactly as numpy computes
+// _interp_matrix (ingest.py:111-125): every operation separately rounded.
+int images_upload(sdnn_net* net, int64_t n, int side, const uint8_t* pixels, int t, sdnn_batch* b) {
+    static const int kSides[] = {32, 64, 128, 256};  // ingest.TARGET_SIDES
+    if (std::find(std::begin(kSides), std::end(kSides), t) == std::end(kSides))
+        return fail(SDNN_ERR_PARAMETER, "target side %d is not one of (32, 64, 128, 256)", t);
+    if (side < 1 || n < 0 || (n > 0 && !pixels)) return fail(SDNN_ERR_PARAMETER, "bad image set");
+    if ((int64_t)t * t != net->n)
+        return fail(SDNN_ERR_SHAPE, "images resize to %d columns but the network has %lld neurons", t * t,
+                    (long long)net->n);
+    const size_t smem = ((size_t)side * side + (size_t)t * side) * sizeof(double);
+    if (smem > 200 * 1024) return fail(SDNN_ERR_CAPACITY, "images of side %d are too large to resample", side);
+    std::vector<int2> taps(t);
+    std::vector<double2> w(t);
+    const volatile double ratio = (double)side / (double)t;
+    for (int i = 0; i < t; ++i) {
+        volatile double x = ((double)i + 0.5) * ratio;
+        x = x - 0.5;
+        const double x0 = std::floor(x);
+        const volatile double frac = x - x0;
+        const volatile double wlo = 1.0 - frac;
+        const int64_t a = (int64_t)x0;
+        const int lo = (int)std::min<int64_t>(std::max<int64_t>(a, 0), side - 1);
+        const int hi = (int)std::min<int64_t>(std::max<int64_t>(a + 1, 0), side - 1);
+        if (lo == hi) {
+            volatile double one = 0.0 + wlo;
+            one = one + frac;  // np.add.at into the same entry
+            taps[i] = make_int2(lo, -1);
+            w[i] = make_double2(one, 0.0);
+        } else {
+            taps[i] = make_int2(lo, hi);
+            w[i] = make_double2(wlo, frac);
+        }
+    }
+    cudaStream_t st = net->stream;
+    b->n_rows = n;
+    b->n_cols = (int64_t)t * t;
+    b->col_bytes = b->n_cols <= 65536 ? 2 : 4;
+    b->vals = nullptr;
+    b->finite = true;
+    const int words = t * t / 32;
+    uint8_t* dpix = nullptr;
+    int2* dtaps = nullptr;
+    double2* dw = nullptr;
+    uint32_t* bits = nullptr;
+    int64_t* cnt = nullptr;
+    const int64_t npix = n * side * side;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&b->off), (n + 1) * sizeof(int64_t), st));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&dpix), std::max<int64_t>(npix, 1), st));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&dtaps), t * sizeof(int2), st));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&dw), t * sizeof(double2), st));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&bits), std::max<int64_t>(n * words, 1) * 4, st));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&cnt), std::max<int64_t>(n, 1) * 8, st));
+    if (npix) CK(cudaMemcpyAsync(dpix, pixels, npix, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dtaps, taps.data(), t * sizeof(int2), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dw, w.data(), t * sizeof(double2), cudaMemcpyHostToDevice, st));
+    b->h2d_bytes = npix + t * (int64_t)(sizeof(int2) + sizeof(double2));
+    CK(cudaMemsetAsync(b->off, 0, 8, st));
+    int64_t nnz = 0;
+    if (n > 0) {
+        CK(cudaFuncSetAttribute((const void*)resize_bits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+        const int grid = (int)std::min<int64_t>(n, (int64_t)net->sm_count * 8);
+        resize_bits_kernel<<<grid, 256, smem, st>>>(dpix, n, side, t, dtaps, dw, bits, cnt);
+        CK(cudaGetLastError());
+        size_t tmp_bytes = 0;
+        CK(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, cnt, b->off + 1, (int)n, st));
+        if (tmp_bytes > net->cub_cap) {
+            if (net->cub_tmp) CK(cudaFree(net->cub_tmp));
+            CK(cudaMalloc(&net->cub_tmp, tmp_bytes));
+            net->cub_cap = tmp_bytes;
+        }
+        CK(cub::DeviceScan::InclusiveSum(net->cub_tmp, tmp_bytes, cnt, b->off + 1, (int)n, st));
+        CK(cudaMemcpyAsync(&nnz, b->off + n, 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    b->nnz = nnz;
+    CK(cudaMallocAsync(&b->cols, std::max<int64_t>(nnz, 1) * b->col_bytes, st));
+    if (nnz > 0) {
+        const int grid = (int)std::min<int64_t>(n, (int64_t)net->sm_count * 8);
+        if (b->col_bytes == 2)
+            bits_to_cols_kernel<uint16_t><<<grid, 256, 0, st>>>(bits, n, words, b->off,
+                                                                reinterpret_cast<uint16_t*>(b->cols));
+        else
+            bits_to_cols_kernel<int32_t><<<grid, 256, 0, st>>>(bits, n, words, b->off,
+                                                               reinterpret_cast<int32_t*>(b->cols));
+        CK(cudaGetLastError());
+    }
+    CK(cudaFreeAsync(dpix, st));
+    CK(cudaFreeAsync(dtaps, st));
+    CK(cudaFreeAsync(dw, st));
+    CK(cudaFreeAsync(bits, st));
+    CK(cudaFreeAsync(cnt, st));
+    CK(cudaStreamSynchronize(st));
     return SDNN_OK;
 }
 
@@ -1025,7 +1285,14 @@ int infer_streamed(sdnn_net* net, int64_t n_rows, const int64_t* off, const int6
         }
         sdnn_result part;
         rc = run_impl<T>(net, g.b, ymax, 0, L, want_y, 1, net->n, net->n, &part);
-        if (rc == SDNN_OK) {
+        if (rc == SDNN_OK && want_y && S > 1) rc = y_to_host(&part);
+        if (rc == SDNN_OK && S == 1) {  // one segment: the result is the part (Y may stay on the device)
+            const double keep_wall = res->wall_ms;
+            std::swap(*res, part);
+            res->wall_ms = keep_wall;
+            res->segments = 1;
+            res->h2d_bytes = g.b->h2d_bytes;
+        } else if (rc == SDNN_OK) {
             merge_part(res, part, g.r0, want_y);
             res->h2d_bytes += g.b->h2d_bytes;
         }
@@ -1045,7 +1312,7 @@ int infer_streamed(sdnn_net* net, int64_t n_rows, const int64_t* off, const int6
             }
         return fail(SDNN_ERR_CAPACITY, "streamed upload stopped early");
     }
-    if (rc == SDNN_OK && want_y) res->have_y = true;
+    if (rc == SDNN_OK && want_y && S > 1) res->have_y = true;
     return rc;
 }
 
@@ -1225,6 +1492,53 @@ int sdnn_batch_upload(sdnn_net* net, int64_t n_rows, const int64_t* y_off, const
     return SDNN_OK;
 }
 
+int sdnn_batch_from_images(sdnn_net* net, int64_t n_images, int32_t side, const uint8_t* pixels,
+                           int32_t target_side, sdnn_batch** out) {
+    if (!net || !out) return fail(SDNN_ERR_PARAMETER, "null argument");
+    if (n_images >= (1LL << 31)) return fail(SDNN_ERR_CAPACITY, "batch of %lld rows exceeds int32 row ids", (long long)n_images);
+    if (int rc = set_device(net)) return rc;
+    sdnn_batch* b = new sdnn_batch;
+    b->net = net;
+    if (int rc = images_upload(net, n_images, side, pixels, target_side, b)) {
+        free_batch(b);
+        return rc;
+    }
+    *out = b;
+    return SDNN_OK;
+}
+
+int sdnn_batch_nnz(const sdnn_batch* b, int64_t* nnz) {
+    if (!b || !nnz) return fail(SDNN_ERR_PARAMETER, "null argument");
+    *nnz = b->nnz;
+    return SDNN_OK;
+}
+
+int sdnn_batch_csr(const sdnn_batch* b, int64_t* off, int64_t* cols, double* vals) {
+    if (!b || !off) return fail(SDNN_ERR_PARAMETER, "null argument");
+    if (int rc = set_device(b->net)) return rc;
+    cudaStream_t st = b->net->stream;
+    CK(cudaMemcpyAsync(off, b->off, (b->n_rows + 1) * 8, cudaMemcpyDeviceToHost, st));
+    std::vector<char> c((size_t)std::max<int64_t>(b->nnz, 1) * b->col_bytes);
+    std::vector<char> v;
+    if (b->nnz) CK(cudaMemcpyAsync(c.data(), b->cols, b->nnz * b->col_bytes, cudaMemcpyDeviceToHost, st));
+    const int elem = b->net->dtype == SDNN_F64 ? 8 : 4;
+    if (b->vals && b->nnz) {
+        v.resize((size_t)b->nnz * elem);
+        CK(cudaMemcpyAsync(v.data(), b->vals, b->nnz * elem, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    for (int64_t i = 0; i < b->nnz; ++i) {
+        if (cols)
+            cols[i] = b->col_bytes == 2 ? (int64_t)reinterpret_cast<const uint16_t*>(c.data())[i]
+                                        : (int64_t)reinterpret_cast<const int32_t*>(c.data())[i];
+        if (vals)
+            vals[i] = !b->vals ? 1.0
+                      : elem == 8 ? reinterpret_cast<const double*>(v.data())[i]
+                                  : (double)reinterpret_cast<const float*>(v.data())[i];
+    }
+    return SDNN_OK;
+}
+
 void sdnn_batch_free(sdnn_batch* b) {
     if (b && b->net) cudaSetDevice(b->net->device);
     free_batch(b);
@@ -1357,13 +1671,22 @@ int sdnn_result_launches(const sdnn_result* r, int64_t* n) {
 int sdnn_result_y_nnz(sdnn_result* r, int64_t* nnz) {
     if (!r || !nnz) return fail(SDNN_ERR_PARAMETER, "null argument");
     if (!r->have_y) return fail(SDNN_ERR_PARAMETER, "result was produced without Y (use sdnn_run_y / sdnn_infer)");
-    *nnz = r->off.empty() ? 0 : r->off.back();
+    *nnz = r->d_off ? r->d_nnz : (r->off.empty() ? 0 : r->off.back());
     return SDNN_OK;
 }
 
 int sdnn_result_y_csr(sdnn_result* r, int64_t* off, int64_t* cols, double* vals) {
     if (!r || !off) return fail(SDNN_ERR_PARAMETER, "null argument");
     if (!r->have_y) return fail(SDNN_ERR_PARAMETER, "result was produced without Y");
+    if (r->d_off) {  // device-held Y: straight into the caller's buffers
+        CK(cudaSetDevice(r->device));
+        if (int rc = d2h_large(off, r->d_off, (r->n_rows + 1) * 8)) return rc;
+        if (r->d_nnz && cols)
+            if (int rc = d2h_large(cols, r->d_cols, r->d_nnz * 8)) return rc;
+        if (r->d_nnz && vals)
+            if (int rc = d2h_large(vals, r->d_vals, r->d_nnz * 8)) return rc;
+        return SDNN_OK;
+    }
     memcpy(off, r->off.data(), r->off.size() * sizeof(int64_t));
     const size_t nnz = r->cols.size();
     for (size_t i = 0; i < nnz; ++i) cols[i] = r->cols[i];

@@ -1116,6 +1116,174 @@ __global__ void extract_kernel(const T* __restrict__ slab, const uint2* __restri
     }
 }
 
+// Final Y straight into the reference's layout on the device (SURVEY.md 8f
+// rank 2): canonical CSR in batch-row order, int64 columns, float64 values.
+// row_counts_kernel scatters each live row's entry count (extract_kernel's
+// count pass) to its batch row; after a scan of those, extract_rows_kernel
+// writes every live tile's rows at their offsets.  Tiles hold rows in
+// ascending batch order and each lane walks its lines in ascending column
+// order, so every row comes out sorted.
+template <typename T>
+__global__ void row_counts_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ rowid,
+                                  const uint32_t* __restrict__ alive, int64_t n_lanes, int64_t* __restrict__ rowcnt) {
+    constexpr int TR = tile_rows<T>(), AW = alive_words<T>();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_lanes;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t row = rowid[i];
+        if (row < 0) continue;
+        const int64_t t = i / TR;
+        const int r = (int)(i % TR);
+        const bool live = (alive[t * AW + r / 32] >> (r % 32)) & 1u;
+        rowcnt[row] = live ? counts[i] : 0;
+    }
+}
+
+template <typename T>
+__global__ void extract_rows_kernel(const T* __restrict__ slab, const uint2* __restrict__ meta, int ld, int n_cols,
+                                    int n_tiles, const uint32_t* __restrict__ alive,
+                                    const int32_t* __restrict__ rowid, const int64_t* __restrict__ off,
+                                    int64_t* __restrict__ cols_out, double* __restrict__ vals_out) {
+    constexpr int RPL = rows_per_lane<T>(), TR = tile_rows<T>(), AW = alive_words<T>();
+    const int lane = threadIdx.x & 31;
+    const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int n_warps = (gridDim.x * blockDim.x) >> 5;
+    const unsigned lbit = 1u << lane;
+    for (int t = warp_global; t < n_tiles; t += n_warps) {
+        if (alive[(size_t)t * AW + AW - 1] == 0u) continue;  // dead tile: its slab is stale
+        const T* s = slab + (size_t)t * ld * TR;
+        const uint2* m = meta + (size_t)t * ld;
+        int64_t at[RPL];
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+            const int r = lane * RPL + q;
+            const int32_t row = rowid[(size_t)t * TR + r];
+            const bool live = row >= 0 && ((alive[(size_t)t * AW + r / 32] >> (r % 32)) & 1u);
+            at[q] = live ? off[row] : -1;
+        }
+        for (int k = 0; k < n_cols; ++k) {
+            const uint2 mk = m[k];
+            if (!(mk.x & lbit)) continue;
+            const T* sec = s + (size_t)(mk.y + sector_pos(mk.x, lane)) * RPL;
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) {
+                const T v = sec[q];
+                if (v != T(0) && at[q] >= 0) {
+                    cols_out[at[q]] = k;
+                    vals_out[at[q]] = (double)v;
+                    ++at[q];
+                }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------- image preprocessing
+// ingest.resize_threshold_flatten (ingest.py:128-156) on the device: pixels
+// / 255, bilinear resample h @ img @ h.T with the half-pixel-centre,
+// edge-clamped interpolation matrix h (ingest.py:111-125, at most two taps
+// per output), threshold >= 0.5, flatten row-major (column r * t + c).  The
+// reference evaluates both products with BLAS dgemm, whose kernels
+// accumulate every output as one fused multiply-add chain over the inner
+// index in ascending order from 0; a zero tap adds +0 and changes nothing,
+// so each output is  fma(w_hi, x_hi, w_lo * x_lo)  (one rounded product
+// when both taps coincide at an edge).  Pinned against the reference on
+// 2,000 synthetic digits at every target side (tests/golden/images_*).
+// taps[i] = {lo, hi} (hi < 0: single tap), w[i] = {w_lo, w_hi}, computed on
+// the host exactly as numpy does.
+__device__ __forceinline__ double two_tap(double xlo, double xhi, double wlo, double whi, bool two) {
+    const double acc = __dmul_rn(wlo, xlo);
+    return two ? __fma_rn(whi, xhi, acc) : acc;
+}
+
+// One block per image: pass 1 (t x side) into shared memory, pass 2 writes
+// the t*t threshold bits as 32-bit words and the image's entry count.
+__global__ void resize_bits_kernel(const uint8_t* __restrict__ pix, int64_t n, int side, int t,
+                                   const int2* __restrict__ taps, const double2* __restrict__ w,
+                                   uint32_t* __restrict__ bits, int64_t* __restrict__ count) {
+    extern __shared__ __align__(16) unsigned char rsm[];
+    double* img = reinterpret_cast<double*>(rsm);  // [side][side]
+    double* tmp = img + side * side;                // [t][side]
+    __shared__ int s_cnt[32];
+    const int words = t * t / 32;
+    for (int64_t im = blockIdx.x; im < n; im += gridDim.x) {
+        const uint8_t* P = pix + im * side * side;
+        for (int i = threadIdx.x; i < side * side; i += blockDim.x) img[i] = __ddiv_rn((double)P[i], 255.0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < t * side; e += blockDim.x) {
+            const int i = e / side, b = e % side;
+            const int2 tp = taps[i];
+            const double2 ww = w[i];
+            tmp[e] = two_tap(img[tp.x * side + b], img[max(tp.y, 0) * side + b], ww.x, ww.y, tp.y >= 0);
+        }
+        __syncthreads();
+        int c = 0;
+        for (int q = threadIdx.x; q < words; q += blockDim.x) {
+            const int i = (q * 32) / t, j0 = (q * 32) % t;
+            const double* row = tmp + i * side;
+            uint32_t v = 0u;
+#pragma unroll 4
+            for (int u = 0; u < 32; ++u) {
+                const int2 tp = taps[j0 + u];
+                const double2 ww = w[j0 + u];
+                const double x = two_tap(row[tp.x], row[max(tp.y, 0)], ww.x, ww.y, tp.y >= 0);
+                v |= (x >= 0.5 ? 1u : 0u) << u;
+            }
+            bits[im * words + q] = v;
+            c += __popc(v);
+        }
+        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if ((threadIdx.x & 31) == 0) s_cnt[threadIdx.x >> 5] = c;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int64_t s = 0;
+            for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += s_cnt[k];
+            count[im] = s;
+        }
+        __syncthreads();
+    }
+}
+
+// Threshold bits -> CSR columns (ascending), one block per image; cols are
+// uint16 when t*t <= 65536 else int32 (the engine's device batch layout).
+template <typename C>
+__global__ void bits_to_cols_kernel(const uint32_t* __restrict__ bits, int64_t n, int words,
+                                    const int64_t* __restrict__ off, C* __restrict__ cols) {
+    __shared__ int s_warp[32];
+    __shared__ int64_t s_base;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int64_t im = blockIdx.x; im < n; im += gridDim.x) {
+        if (threadIdx.x == 0) s_base = off[im];
+        __syncthreads();
+        const uint32_t* B = bits + im * words;
+        for (int q0 = 0; q0 < words; q0 += blockDim.x) {
+            const int q = q0 + threadIdx.x;
+            const uint32_t v = q < words ? B[q] : 0u;
+            const int c = __popc(v);
+            int x = c;  // inclusive scan over the block
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) s_warp[warp] = x;
+            __syncthreads();
+            if (warp == 0) {
+                int s = lane < nw ? s_warp[lane] : 0;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, s, o);
+                    if (lane >= o) s += y;
+                }
+                if (lane < nw) s_warp[lane] = s;
+            }
+            __syncthreads();
+            int64_t at = s_base + (warp ? s_warp[warp - 1] : 0) + x - c;
+            for (uint32_t m = v; m; m &= m - 1) cols[at++] = (C)(q * 32 + __ffs(m) - 1);
+            __syncthreads();
+            if (threadIdx.x == 0) s_base += s_warp[nw - 1];
+            __syncthreads();
+        }
+    }
+}
+
 // ------------------------------------------------------------ weight ingest
 // CSR by input (the reference's LayerWeights, model.py:128-139) -> ELL by
 // output on the device.  The host only narrows the

@@ -157,21 +157,37 @@ class RunResult:
 class DeviceBatch:
     """Y0 staged in HBM (device CSR)."""
 
-    def __init__(self, net: "DeviceNetwork", n_rows, off, cols, vals):
+    def __init__(self, net: "DeviceNetwork", n_rows, off, cols, vals, handle=None):
         self.net = net
         self.n_rows = int(n_rows)
         self.handle = ctypes.c_void_p()
-        _lib.check(_lib.lib().sdnn_batch_upload(
-            net.handle, self.n_rows, _lib.ptr(_nonempty(off, np.int64)),
-            _lib.ptr(_nonempty(cols, np.int64)), _lib.ptr(_nonempty(vals, np.float64)),
-            ctypes.byref(self.handle)))
+        if handle is not None:  # staged by another entry point (sdnn_batch_from_images)
+            self.handle = handle
+        else:
+            _lib.check(_lib.lib().sdnn_batch_upload(
+                net.handle, self.n_rows, _lib.ptr(_nonempty(off, np.int64)),
+                _lib.ptr(_nonempty(cols, np.int64)), _lib.ptr(_nonempty(vals, np.float64)),
+                ctypes.byref(self.handle)))
         b = ctypes.c_int64()
         _lib.check(_lib.lib().sdnn_batch_h2d_bytes(self.handle, ctypes.byref(b)))
         self.h2d_bytes = b.value
+        net._batches.add(self)  # freed before the network that owns its stream
+
+    def to_csr(self):
+        """(off, cols, vals) of the staged batch, int64/int64/float64."""
+        L = _lib.lib()
+        nnz = ctypes.c_int64()
+        _lib.check(L.sdnn_batch_nnz(self.handle, ctypes.byref(nnz)))
+        off = np.zeros(self.n_rows + 1, np.int64)
+        cols = np.zeros(max(nnz.value, 1), np.int64)
+        vals = np.zeros(max(nnz.value, 1), np.float64)
+        _lib.check(L.sdnn_batch_csr(self.handle, _lib.ptr(off), _lib.ptr(cols), _lib.ptr(vals)))
+        return off, cols[:nnz.value], vals[:nnz.value]
 
     def close(self):
         if self.handle:
-            _lib.lib().sdnn_batch_free(self.handle)
+            if self.net.handle:  # a closed network already freed it
+                _lib.lib().sdnn_batch_free(self.handle)
             self.handle = ctypes.c_void_p()
 
     def __del__(self):
@@ -205,6 +221,7 @@ class DeviceNetwork:
                                               ctypes.byref(self.handle)))
         self.n_layers = 0
         self.lock = threading.Lock()  # one handle, one host thread at a time
+        self._batches = weakref.WeakSet()
 
     @classmethod
     def from_model(cls, model, device: int = 0, dtype: str = "f32") -> "DeviceNetwork":
@@ -271,6 +288,20 @@ class DeviceNetwork:
             raise ShapeError(f"input has {n_cols} columns but the model expects {self.n} neurons")
         return DeviceBatch(self, n_rows, off, cols, vals)
 
+    def upload_images(self, images, target_side: int) -> DeviceBatch:
+        """ingest.resize_threshold_flatten (ingest.py:128-156) on the device:
+        an ImageSet (count, side, uint8 pixels) resampled, thresholded and
+        flattened straight into a staged batch; only the raw pixels cross
+        PCIe."""
+        pix = np.ascontiguousarray(getattr(images, "pixels", images), np.uint8)
+        if pix.ndim != 3 or pix.shape[1] != pix.shape[2]:
+            raise ParameterError("images must be a (count, side, side) uint8 array")
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().sdnn_batch_from_images(
+            self.handle, pix.shape[0], pix.shape[1], _lib.ptr(_nonempty(pix.reshape(-1), np.uint8)),
+            int(target_side), ctypes.byref(h)))
+        return DeviceBatch(self, pix.shape[0], None, None, None, handle=h)
+
     def upload_csr(self, n_rows, off, cols, vals) -> DeviceBatch:
         return DeviceBatch(self, n_rows, np.ascontiguousarray(off, np.int64),
                            np.ascontiguousarray(cols, np.int64), np.ascontiguousarray(vals, np.float64))
@@ -318,6 +349,8 @@ class DeviceNetwork:
 
     def close(self):
         if self.handle:
+            for b in list(self._batches):  # batches live in this network's stream and pool
+                b.close()
             _lib.lib().sdnn_net_destroy(self.handle)
             self.handle = ctypes.c_void_p()
 
@@ -352,9 +385,9 @@ def _collect(h, n_rows: int, want_y: bool) -> RunResult:
     if want_y:
         nnz = ctypes.c_int64()
         _lib.check(L.sdnn_result_y_nnz(h, ctypes.byref(nnz)))
-        off = np.zeros(n_rows + 1, np.int64)
-        cols = np.zeros(max(nnz.value, 1), np.int64)
-        vals = np.zeros(max(nnz.value, 1), np.float64)
+        off = np.empty(n_rows + 1, np.int64)
+        cols = np.empty(max(nnz.value, 1), np.int64)  # filled by the copy: no zeroing pass
+        vals = np.empty(max(nnz.value, 1), np.float64)
         _lib.check(L.sdnn_result_y_csr(h, _lib.ptr(off), _lib.ptr(cols), _lib.ptr(vals)))
         y = (off, cols[:nnz.value], vals[:nnz.value])
     return RunResult(cats, live, L.sdnn_result_device_ms(h), L.sdnn_result_wall_ms(h),

@@ -235,6 +235,29 @@ def test_wave_splitting_does_not_change_bits(env):
     assert O.CSR(y0.n_rows, w.n, *res.y).identical(want)
 
 
+@pytest.mark.parametrize("dtype,prec", [("f64", 64), ("f32", 32)])
+def test_device_y_matches_host_assembly_and_oracle(env, dtype, prec):
+    """Final Y materialised on the device (row-ordered int64/float64 CSR,
+    SURVEY 8f rank 2) == the host assembly path == multi-wave runs == the
+    oracle, on a workload where some rows and whole tiles die."""
+    w, y0, layers = permunion_case(4096, 5, 700, 0.12)  # 20 of 700 rows survive
+    want = O.infer(layers, [w.bias] * w.layers, y0, precision=prec, threads=8)
+    net = E.DeviceNetwork(w.n, 0, dtype)
+    net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias)
+    batch = net.upload_csr(y0.n_rows, y0.off, y0.cols, y0.vals)
+    dev = net.run(batch, w.ymax, want_y=True)
+    assert O.CSR(y0.n_rows, w.n, *dev.y).identical(want)
+    assert 0 < dev.categories.size < y0.n_rows
+    env["SDNN_HOST_Y"] = "1"
+    host = net.run(batch, w.ymax, want_y=True)
+    env["SDNN_HOST_Y"] = "0"
+    env["SDNN_WAVE_ROWS"] = "300"
+    waves = net.run(batch, w.ymax, want_y=True)
+    for r in (host, waves):
+        assert all(np.array_equal(a, b) for a, b in zip(r.y, dev.y))
+    net.close()
+
+
 def test_e2e_host_call_matches_device_resident_run():
     w, y0, layers = permunion_case(1024, 8, 300, 0.125)
     net = E.DeviceNetwork(w.n, 0, "f32")
@@ -516,3 +539,68 @@ def test_layer_buffers_replicate_a_network():
         assert np.array_equal(a.categories, b.categories)
         src.close()
         dst.close()
+
+
+# ------------------------------------------- image preprocessing (8f rank 4)
+
+def test_device_resize_matches_reference_golden():
+    """sdnn_batch_from_images == the reference's resize_threshold_flatten on
+    images holding values within 1e-9 of the threshold, at every side."""
+    from paper_1909_05631_b200 import ingest as I
+
+    z = np.load(goldens.GOLDEN / "images.npz")
+    for t in (int(v) for v in z["sides"]):
+        fb = I.resize_threshold_flatten(z["pixels"], t)
+        d = fb.data
+        assert np.array_equal(np.asarray(d.row_offsets), z[f"off{t}"]), t
+        want = np.unpackbits(z[f"mask{t}"], axis=1)[:, :t * t].astype(bool)
+        rows = np.repeat(np.arange(want.shape[0]), np.diff(z[f"off{t}"]))
+        got = np.zeros_like(want)
+        got[rows, np.asarray(d.col_indices)] = True
+        assert np.array_equal(got, want), t
+        assert np.all(np.asarray(d.values) == 1.0)
+
+
+@pytest.mark.parametrize("side,t", [(28, 32), (28, 256), (64, 32), (17, 128), (40, 64)])
+def test_device_resize_matches_oracle_other_sides(side, t):
+    from paper_1909_05631_b200 import ingest as I
+
+    rng = np.random.default_rng(side * 1000 + t)
+    pix = rng.integers(0, 256, size=(37, side, side), dtype=np.uint8)
+    pix[::3] = (pix[::3] > 128) * 255  # hard edges: exact 0.5 crossings
+    want = O.resize_threshold_flatten(pix, t)
+    d = I.resize_threshold_flatten(pix, t).data
+    assert np.array_equal(np.asarray(d.row_offsets), want.off)
+    assert np.array_equal(np.asarray(d.col_indices), want.cols)
+
+
+def test_device_resize_errors_and_empty():
+    from paper_1909_05631_b200 import ingest as I
+
+    with pytest.raises(ParameterError):
+        I.resize_threshold_flatten(np.zeros((2, 28, 28), np.uint8), 100)
+    net = E.DeviceNetwork(1024, 0, "f32")
+    with pytest.raises(ShapeError):
+        net.upload_images(np.zeros((2, 28, 28), np.uint8), 64)
+    b = net.upload_images(np.zeros((0, 28, 28), np.uint8), 32)
+    off, cols, _ = b.to_csr()
+    assert off.tolist() == [0] and cols.size == 0
+    b.close()
+    net.close()
+
+
+@pytest.mark.parametrize("dtype,prec", [("f64", 64), ("f32", 32)])
+def test_images_to_categories_on_device(dtype, prec):
+    """Raw images -> device resize -> all layers: the same result as the
+    reference-format host batch (oracle resize + oracle engine)."""
+    z = np.load(goldens.GOLDEN / "images.npz")
+    w = W.CONFIGS["C1"].with_(layers=6, batch=int(z["pixels"].shape[0]), value=0.1)
+    layers = [O.CSR(w.n, w.n, *W.layer_csr(w, l)) for l in range(w.layers)]
+    y0 = O.resize_threshold_flatten(z["pixels"], 32)
+    want = O.infer(layers, [w.bias] * w.layers, y0, w.ymax, precision=prec, threads=4)
+    net = E.DeviceNetwork(w.n, 0, dtype)
+    net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias)
+    res = net.run(net.upload_images(z["pixels"], 32), w.ymax, want_y=True)
+    assert O.CSR(y0.n_rows, w.n, *res.y).identical(want)
+    assert np.array_equal(res.categories, O.categorize(want))
+    net.close()

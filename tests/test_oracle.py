@@ -141,3 +141,19 @@ class TestGoldens:
         a = O.infer([w] * 5, [-0.25] * 5, y, precision=64)
         b = O.infer([w] * 5, [-0.25] * 5, y, precision=32)
         assert a.identical(b)
+
+
+# ------------------------------------------- image preprocessing (8f rank 4)
+
+def test_oracle_resize_matches_reference_golden():
+    """The C restatement of ingest.resize_threshold_flatten reproduces the
+    reference's output on images chosen because they hold values within
+    1e-9 of the threshold (where a reordered or unfused sum flips pixels)."""
+    z = np.load(goldens.GOLDEN / "images.npz")
+    for t in z["sides"]:
+        t = int(t)
+        m = O.resize_threshold_masks(z["pixels"], t)
+        want = np.unpackbits(z[f"mask{t}"], axis=1)[:, :t * t].astype(bool)
+        assert np.array_equal(m, want), t
+        csr = O.resize_threshold_flatten(z["pixels"], t)
+        assert np.array_equal(csr.off, z[f"off{t}"]), t
