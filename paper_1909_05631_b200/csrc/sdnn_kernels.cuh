@@ -439,6 +439,19 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_kernel(const int64_t*
 // lines is assembled in shared memory with atomicOr, then each nonzero line
 // is appended to the tile's heap (one 32-byte unit) with meta {all lanes,
 // heap index}.  Layer 1 then reads 32 bytes per gathered line instead of 1 KB.
+// Staging swizzle: a warp's lanes hold one row's entries (different lines,
+// the same word of each), so without it the words of lines kk and kk+4 share
+// a bank; XOR-ing the word with higher line bits spreads a warp's atomics
+// over all 32 banks.
+#ifndef SDNN_BIN_SWZ
+#define SDNN_BIN_SWZ 1
+#endif
+template <int W>
+__device__ __forceinline__ int bin_swz(int k) {
+    constexpr int shift = W == 8 ? 2 : (W == 4 ? 3 : 5);
+    return SDNN_BIN_SWZ ? (k >> shift) & (W - 1) : 0;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kDensifyThreads) densify_bin_kernel(const int64_t* __restrict__ csr_off,
                                                                       const void* __restrict__ csr_cols,
@@ -499,7 +512,8 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_bin_kernel(const int6
                 for (int i = 0; i < RW; ++i) {
                     if (cb[i] < k0 + kn) {
                         const int r = warp + i * NW;
-                        atomicOr(&stage[(cb[i] - k0) * W + r / 32], 1u << (r % 32));
+                        const int kk = cb[i] - k0;
+                        atomicOr(&stage[kk * W + ((r / 32) ^ bin_swz<W>(kk))], 1u << (r % 32));
                         cb[i] = INT32_MAX;
                     }
                 }
@@ -524,8 +538,9 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_bin_kernel(const int6
                 uint32_t any = 0u;
 #pragma unroll
                 for (int q = 0; q < W; ++q) {
-                    wv[q] = stage[k * W + q];
-                    stage[k * W + q] = 0u;
+                    const int at = k * W + (q ^ bin_swz<W>(k));
+                    wv[q] = stage[at];
+                    stage[at] = 0u;
                     any |= wv[q];
                 }
                 if (any) {
