@@ -110,6 +110,12 @@ void sdnn_batch_free(sdnn_batch *batch);
  * network's neuron count. */
 int sdnn_batch_from_images(sdnn_net *net, int64_t n_images, int32_t side, const uint8_t *pixels,
                            int32_t target_side, sdnn_batch **out);
+/* The pipeline hand-off (engine._infer_pipeline, engine.py:254-297): the
+ * final Y of a run made with sdnn_run_y becomes the staged input of the
+ * next layer range on `net` without leaving the device -- a device-to-device
+ * copy, or a peer copy over NVLink when `net` is on another GPU.  ShapeError
+ * unless the result's width equals the network's neuron count. */
+int sdnn_batch_from_result(sdnn_net *net, const sdnn_result *result, sdnn_batch **out);
 /* A staged batch back as host CSR (values 1.0 for a binary batch; cols and
  * vals may be null): query nnz first. */
 int sdnn_batch_nnz(const sdnn_batch *batch, int64_t *nnz);

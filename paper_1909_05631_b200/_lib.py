@@ -39,6 +39,7 @@ SIGNATURES = [
     ("sdnn_batch_free", None, [vp]),
     ("sdnn_batch_from_images", cint, [vp, i64, i32, vp, i32, P(vp)]),
     ("sdnn_batch_nnz", cint, [vp, P(i64)]),
+    ("sdnn_batch_from_result", cint, [vp, vp, P(vp)]),
     ("sdnn_batch_csr", cint, [vp, vp, vp, vp]),
     ("sdnn_batch_h2d_bytes", cint, [vp, P(i64)]),
     ("sdnn_run", cint, [vp, vp, dbl, i64, i64, P(vp)]),

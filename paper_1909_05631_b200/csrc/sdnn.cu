@@ -1492,6 +1492,96 @@ int sdnn_batch_upload(sdnn_net* net, int64_t n_rows, const int64_t* y_off, const
     return SDNN_OK;
 }
 
+int sdnn_batch_from_result(sdnn_net* net, const sdnn_result* r, sdnn_batch** out) {
+    if (!net || !r || !out) return fail(SDNN_ERR_PARAMETER, "null argument");
+    if (!r->have_y) return fail(SDNN_ERR_PARAMETER, "result was produced without Y (use sdnn_run_y)");
+    if (r->n_cols != net->n)
+        return fail(SDNN_ERR_SHAPE, "result has %lld columns but the network has %lld neurons", (long long)r->n_cols,
+                    (long long)net->n);
+    if (int rc = set_device(net)) return rc;
+    sdnn_batch* b = new sdnn_batch;
+    b->net = net;
+    int rc = SDNN_OK;
+    if (!r->d_off) {  // Y assembled on the host (multi-wave run): upload it
+        rc = net->dtype == SDNN_F64
+                 ? upload_csr<double>(net, r->n_rows, r->off.data(), r->cols.data(), r->vals.data(), net->n, b, true)
+                 : upload_csr<float>(net, r->n_rows, r->off.data(), r->cols.data(), r->vals.data(), net->n, b, true);
+        if (rc) {
+            free_batch(b);
+            return rc;
+        }
+        *out = b;
+        return SDNN_OK;
+    }
+    cudaStream_t st = net->stream;
+    const int64_t n = r->n_rows, nnz = r->d_nnz;
+    b->n_rows = n;
+    b->nnz = nnz;
+    b->n_cols = net->n;
+    b->col_bytes = net->n <= 65536 ? 2 : 4;
+    const int elem = net->dtype == SDNN_F64 ? 8 : 4;
+    const int64_t* src_off = r->d_off;
+    const int64_t* src_cols = r->d_cols;
+    const double* src_vals = r->d_vals;
+    int64_t* tcols = nullptr;
+    double* tvals = nullptr;
+    int* fin = nullptr;
+    auto cleanup = [&]() {
+        if (tcols) cudaFreeAsync(tcols, st);
+        if (tvals) cudaFreeAsync(tvals, st);
+        if (fin) cudaFreeAsync(fin, st);
+    };
+#define CKB(call)                        \
+    do {                                 \
+        cudaError_t e_ = (call);         \
+        if (e_ != cudaSuccess) {         \
+            cleanup();                   \
+            free_batch(b);               \
+            return fail(SDNN_ERR_CAPACITY, "%s failed: %s", #call, cudaGetErrorString(e_)); \
+        }                                \
+    } while (0)
+    CKB(cudaMallocAsync(reinterpret_cast<void**>(&b->off), (n + 1) * 8, st));
+    CKB(cudaMallocAsync(&b->cols, std::max<int64_t>(nnz, 1) * b->col_bytes, st));
+    CKB(cudaMallocAsync(&b->vals, std::max<int64_t>(nnz, 1) * elem, st));
+    CKB(cudaMallocAsync(reinterpret_cast<void**>(&fin), 4, st));
+    if (r->device != net->device) {  // hand-off across GPUs: peer copies (NVLink / NVSwitch)
+        CKB(cudaMallocAsync(reinterpret_cast<void**>(&tcols), std::max<int64_t>(nnz, 1) * 8, st));
+        CKB(cudaMallocAsync(reinterpret_cast<void**>(&tvals), std::max<int64_t>(nnz, 1) * 8, st));
+        CKB(cudaMemcpyPeerAsync(b->off, net->device, src_off, r->device, (n + 1) * 8, st));
+        if (nnz) {
+            CKB(cudaMemcpyPeerAsync(tcols, net->device, src_cols, r->device, nnz * 8, st));
+            CKB(cudaMemcpyPeerAsync(tvals, net->device, src_vals, r->device, nnz * 8, st));
+        }
+        src_cols = tcols;
+        src_vals = tvals;
+    } else {
+        CKB(cudaMemcpyAsync(b->off, src_off, (n + 1) * 8, cudaMemcpyDeviceToDevice, st));
+    }
+    CKB(cudaMemsetAsync(fin, 0xff, 4, st));
+    if (nnz) {
+        const int grid = (int)std::min<int64_t>((nnz + 255) / 256, (int64_t)net->sm_count * 8);
+        if (b->col_bytes == 2 && elem == 4)
+            narrow_csr_kernel<uint16_t, float><<<grid, 256, 0, st>>>(src_cols, src_vals, nnz, (uint16_t*)b->cols, (float*)b->vals, fin);
+        else if (b->col_bytes == 2)
+            narrow_csr_kernel<uint16_t, double><<<grid, 256, 0, st>>>(src_cols, src_vals, nnz, (uint16_t*)b->cols, (double*)b->vals, fin);
+        else if (elem == 4)
+            narrow_csr_kernel<int32_t, float><<<grid, 256, 0, st>>>(src_cols, src_vals, nnz, (int32_t*)b->cols, (float*)b->vals, fin);
+        else
+            narrow_csr_kernel<int32_t, double><<<grid, 256, 0, st>>>(src_cols, src_vals, nnz, (int32_t*)b->cols, (double*)b->vals, fin);
+        CKB(cudaGetLastError());
+    }
+    int hfin = 1;
+    CKB(cudaMemcpyAsync(&hfin, fin, 4, cudaMemcpyDeviceToHost, st));
+    CKB(cudaStreamSynchronize(st));
+#undef CKB
+    b->finite = hfin != 0;
+    b->h2d_bytes = 0;
+    cleanup();
+    CK(cudaStreamSynchronize(st));
+    *out = b;
+    return SDNN_OK;
+}
+
 int sdnn_batch_from_images(sdnn_net* net, int64_t n_images, int32_t side, const uint8_t* pixels,
                            int32_t target_side, sdnn_batch** out) {
     if (!net || !out) return fail(SDNN_ERR_PARAMETER, "null argument");

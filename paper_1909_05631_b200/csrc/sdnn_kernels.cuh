@@ -1192,6 +1192,22 @@ __global__ void extract_rows_kernel(const T* __restrict__ slab, const uint2* __r
     }
 }
 
+// A device-held result (int64 columns, float64 values) -> the engine's
+// staged batch layout (uint16 / int32 columns, T values) for the next layer
+// range: the pipeline hand-off stays on the device (or crosses NVLink).
+template <typename C, typename T>
+__global__ void narrow_csr_kernel(const int64_t* __restrict__ cols, const double* __restrict__ vals, int64_t nnz,
+                                  C* __restrict__ cols_out, T* __restrict__ vals_out, int* __restrict__ finite) {
+    bool fin = true;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x) {
+        cols_out[p] = (C)cols[p];
+        const T v = (T)vals[p];
+        vals_out[p] = v;
+        fin &= isfinite(v);
+    }
+    if (!__all_sync(0xffffffffu, fin) && (threadIdx.x & 31) == 0) atomicAnd(finite, 0);
+}
+
 // ------------------------------------------------- image preprocessing
 // ingest.resize_threshold_flatten (ingest.py:128-156) on the device: pixels
 // / 255, bilinear resample h @ img @ h.T with the half-pixel-centre,

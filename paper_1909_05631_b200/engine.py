@@ -17,8 +17,10 @@ Modes map onto GPUs the way the reference maps them onto threads:
 ``serial`` uses one GPU; ``data_parallel`` splits the batch into contiguous
 row blocks, one per GPU (up to ``workers``), each GPU holding a full weight
 replica, one host thread per GPU (engine.py:237-251); ``pipeline`` runs
-contiguous layer ranges one after another (engine.py:254-297).  Every mode
-produces bit-identical output, as in the reference.
+contiguous layer ranges as stages over ``devices`` (engine.py:254-297), each
+stage's output handed to the next on the device (a peer copy over NVLink
+between GPUs).  Every mode produces bit-identical output, as in the
+reference.
 
 ``dtype="f64"`` (default) is bit-exact with the reference; ``dtype="f32"``
 is the throughput path (same algorithm in float arithmetic).
@@ -318,6 +320,24 @@ class DeviceNetwork:
         finally:
             L.sdnn_result_free(h)
 
+    def run_to_batch(self, batch: DeviceBatch, ymax: float, first_layer: int, n_layers: int,
+                     target: "DeviceNetwork | None" = None) -> DeviceBatch:
+        """Run a layer range and hand its final Y to `target` (this network
+        by default) as a staged batch without leaving the device: the
+        pipeline hand-off (engine.py:254-297), a peer copy over NVLink when
+        `target` lives on another GPU."""
+        L = _lib.lib()
+        h = ctypes.c_void_p()
+        _lib.check(L.sdnn_run_y(self.handle, batch.handle, float(ymax), int(first_layer), int(n_layers),
+                                ctypes.byref(h)))
+        target = target or self
+        try:
+            out = ctypes.c_void_p()
+            _lib.check(L.sdnn_batch_from_result(target.handle, h, ctypes.byref(out)))
+        finally:
+            L.sdnn_result_free(h)
+        return DeviceBatch(target, batch.n_rows, None, None, None, handle=out)
+
     def infer_host(self, y0, ymax: float = DEFAULT_YMAX, want_y: bool = True,
                    segments: int = 0) -> RunResult:
         """End-to-end C-ABI call (sdnn_infer_streamed): host CSR in,
@@ -445,14 +465,28 @@ def _run_block(model, dtype, device, ymax, n_rows, off, cols, vals, ranges):
     with net.lock:
         if ranges == [(0, model.n_layers)]:  # one range: upload streamed behind the run
             return net.infer_csr(n_rows, off, cols, vals, ymax, want_y=True).y
-        for lo, hi in ranges:
-            batch = net.upload_csr(n_rows, off, cols, vals)
+    return _run_stages(model, dtype, [device], ymax, n_rows, off, cols, vals, ranges)
+
+
+def _run_stages(model, dtype, devices, ymax, n_rows, off, cols, vals, ranges):
+    """Pipeline stages (engine._infer_pipeline, engine.py:254-297): layer
+    range i on devices[i % len(devices)]; each stage's final Y becomes the
+    next stage's input on the device (a peer copy over NVLink between GPUs),
+    only the last stage's Y comes back to the host."""
+    nets = [_device_network(model, devices[i % len(devices)], dtype) for i in range(len(ranges))]
+    first = nets[0]
+    with first.lock:
+        batch = first.upload_csr(n_rows, off, cols, vals)
+    for i, (lo, hi) in enumerate(ranges):
+        net = nets[i]
+        with net.lock:
             try:
-                res = net.run(batch, ymax, lo, hi - lo, want_y=True)
+                if i + 1 == len(ranges):
+                    return net.run(batch, ymax, lo, hi - lo, want_y=True).y
+                nxt = net.run_to_batch(batch, ymax, lo, hi - lo, target=nets[i + 1])
             finally:
                 batch.close()
-            off, cols, vals = res.y
-    return off, cols, vals
+        batch = nxt
 
 
 def infer(model, y0, cfg: InferenceConfig | None = None):
@@ -478,7 +512,9 @@ def infer(model, y0, cfg: InferenceConfig | None = None):
     else:
         ranges = [(0, L)]
     devs = _devices(cfg)
-    if len(devs) == 1 or n_rows <= 1:
+    if cfg.mode == "pipeline":  # stages over the configured devices, hand-off on device
+        o, c, v = _run_stages(model, cfg.dtype, devs, cfg.ymax, n_rows, off, cols, vals, ranges)
+    elif len(devs) == 1 or n_rows <= 1:
         o, c, v = _run_block(model, cfg.dtype, devs[0], cfg.ymax, n_rows, off, cols, vals, ranges)
     else:
         per = -(-n_rows // len(devs))

@@ -258,6 +258,36 @@ def test_device_y_matches_host_assembly_and_oracle(env, dtype, prec):
     net.close()
 
 
+@pytest.mark.parametrize("dtype,prec", [("f64", 64), ("f32", 32)])
+@pytest.mark.parametrize("waves", ["0", "150"])
+def test_pipeline_handoff_on_device(env, dtype, prec, waves):
+    """Layer ranges chained through sdnn_batch_from_result (device Y of one
+    range -> staged batch of the next, no host round trip) == one run over
+    all layers == the oracle; with waves the result is host-assembled and
+    the hand-off uploads it instead."""
+    if waves != "0":
+        env["SDNN_WAVE_ROWS"] = waves
+    w, y0, layers = permunion_case(4096, 7, 700, 0.12)
+    want = O.infer(layers, [w.bias] * w.layers, y0, precision=prec, threads=8)
+    net = E.DeviceNetwork(w.n, 0, dtype)
+    net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias)
+    other = E.DeviceNetwork(w.n, 0, dtype)  # a second stage network (same GPU here)
+    other.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias)
+    b = net.upload_csr(y0.n_rows, y0.off, y0.cols, y0.vals)
+    b = net.run_to_batch(b, w.ymax, 0, 2)
+    b = net.run_to_batch(b, w.ymax, 2, 3, target=other)
+    res = other.run(b, w.ymax, 5, 2, want_y=True)
+    assert O.CSR(y0.n_rows, w.n, *res.y).identical(want)
+    with pytest.raises(ShapeError):
+        small = E.DeviceNetwork(1024, 0, dtype)
+        try:
+            net.run_to_batch(net.upload_csr(y0.n_rows, y0.off, y0.cols, y0.vals), w.ymax, 0, 1, target=small)
+        finally:
+            small.close()
+    other.close()
+    net.close()
+
+
 def test_e2e_host_call_matches_device_resident_run():
     w, y0, layers = permunion_case(1024, 8, 300, 0.125)
     net = E.DeviceNetwork(w.n, 0, "f32")
