@@ -1237,7 +1237,9 @@ int infer_streamed(sdnn_net* net, int64_t n_rows, const int64_t* off, const int6
     std::condition_variable cv;
     int ready = 0;  // segments whose upload finished (or failed)
     bool stop = false;
-    const int threads = host_threads();
+    // the caller's OpenMP budget (OMP_NUM_THREADS: bench.py splits the host
+    // cores over the local ranks), one core left for the engine thread
+    const int threads = std::min(omp_get_max_threads(), host_threads());
     std::thread producer([&] {
         cudaSetDevice(net->device);
         omp_set_num_threads(std::max(1, threads - 1));  // one core runs the engine stream
