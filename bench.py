@@ -18,7 +18,9 @@ device time.
 `value`: nominal edges/s (inputs x N x 32 x L / t, challenge.py:131-135) with
 Y0 already resident in HBM, device time from CUDA events on the engine's
 stream.  `e2e`: the same metric through the C ABI with host buffers (H2D of
-Y0 and D2H of the categories inside the timed region).  `roofline`: the
+Y0 and D2H of the categories inside the timed region).  `e2e_images`: the
+same network fed raw 28x28 images resized on the device (the reference's
+ingest.resize_threshold_flatten).  `roofline`: the
 dominant layer launch against measured HBM bandwidth.  `cpu_baseline`: the
 oracle port (a C restatement of the reference engine, oracle/) on the host
 cores over a row sample.  `--impl reference` prints that CPU arm alone.
@@ -313,6 +315,7 @@ def run_ours(args, dist: RankGroup):
     t2 = time.perf_counter()
     b2.close()
     e2e_split = [round((t1 - t0) * 1e3, 1), round((t2 - t1) * 1e3, 1)]
+    images = images_e2e(args, w, net) if dist.world == 1 else None
 
     line = {
         "metric": METRIC,
@@ -370,6 +373,7 @@ def run_ours(args, dist: RankGroup):
         },
         "gpu_launches": launches,
         "wall_ms_per_step": wall_per_step,
+        **({"e2e_images": images} if images else {}),
         "clocks": clk,
         "setup_s": setup_s,
     }
@@ -392,6 +396,46 @@ def run_ours(args, dist: RankGroup):
             "seconds": t_cpu,
         }
     return line
+
+
+def images_e2e(args, w: W.Workload, net):
+    """End to end from raw images: B seeded 28x28
+    uint8 images (W.stroke_images) copied to the device, resized /
+    thresholded / flattened there (sdnn_batch_from_images, the reference's
+    ingest.resize_threshold_flatten) and run through the workload's network,
+    categories back; beside it the same rows through the host-CSR call."""
+    side = int(round(w.n ** 0.5))
+    if args.no_images or side * side != w.n or side not in (32, 64, 128, 256):
+        return None
+    pix = W.stroke_images(w.batch)
+    b = net.upload_images(pix, side)  # warm-up; its CSR feeds the host-CSR comparison
+    off, cols, vals = b.to_csr()
+    b.close()
+    ms = []
+    for _ in range(max(1, min(args.steps, 5)) + 1):
+        t0 = time.perf_counter()
+        b = net.upload_images(pix, side)
+        r = net.run(b, w.ymax)
+        _ = r.categories.copy()
+        ms.append((time.perf_counter() - t0) * 1e3)
+        h2d = b.h2d_bytes
+        b.close()
+    t0 = time.perf_counter()
+    r2 = net.infer_csr(w.batch, off, cols, vals, w.ymax, want_y=False)
+    host_ms = (time.perf_counter() - t0) * 1e3
+    assert np.array_equal(r.categories, r2.categories)
+    e2e_ms = float(np.mean(ms[1:]))
+    return {
+        "workload": f"{w.batch} seeded 28x28 uint8 stroke images resized on the device to "
+                    f"{side}x{side}, then {w.name}'s network",
+        "value": w.edges / (e2e_ms * 1e-3),
+        "unit": UNIT,
+        "ms_per_step": e2e_ms,
+        "h2d_bytes_per_step": int(h2d),
+        "y0_nnz_per_row": float(off[-1]) / w.batch,
+        "categories": int(r.categories.size),
+        "same_rows_from_host_csr_ms": host_ms,
+    }
 
 
 def companions(args, net_cls):
@@ -505,6 +549,7 @@ def main(argv=None):
     ap.add_argument("--p", type=float, default=None)
     ap.add_argument("--cpu-rows", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-images", action="store_true", help="skip the end-to-end-from-images line")
     ap.add_argument("--companions", default="K2:120",
                     help="comma list NAME[:LAYERS] of live companions ('' to skip)")
     args = ap.parse_args(argv)

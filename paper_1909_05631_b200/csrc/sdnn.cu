@@ -911,7 +911,8 @@ int images_upload(sdnn_net* net, int64_t n, int side, const uint8_t* pixels, int
     if ((int64_t)t * t != net->n)
         return fail(SDNN_ERR_SHAPE, "images resize to %d columns but the network has %lld neurons", t * t,
                     (long long)net->n);
-    const size_t smem = ((size_t)side * side + (size_t)t * side) * sizeof(double);
+    const size_t smem = ((size_t)side * side + (size_t)t * side + 256) * sizeof(double) +
+                        (size_t)t * (sizeof(double2) + sizeof(int2));
     if (smem > 200 * 1024) return fail(SDNN_ERR_CAPACITY, "images of side %d are too large to resample", side);
     std::vector<int2> taps(t);
     std::vector<double2> w(t);
@@ -954,7 +955,33 @@ int images_upload(sdnn_net* net, int64_t n, int side, const uint8_t* pixels, int
     CK(cudaMallocAsync(reinterpret_cast<void**>(&dw), t * sizeof(double2), st));
     CK(cudaMallocAsync(reinterpret_cast<void**>(&bits), std::max<int64_t>(n * words, 1) * 4, st));
     CK(cudaMallocAsync(reinterpret_cast<void**>(&cnt), std::max<int64_t>(n, 1) * 8, st));
-    if (npix) CK(cudaMemcpyAsync(dpix, pixels, npix, cudaMemcpyHostToDevice, st));
+    if (npix) {  // pageable pixels -> pinned staging (host threads) -> device, chunk by chunk
+        const int64_t chunk = 16 << 20;
+        const size_t stage_bytes = (size_t)std::min<int64_t>(chunk, npix);
+        if (stage_bytes > net->pinned_cap) {
+            if (net->pinned) CK(cudaFreeHost(net->pinned));
+            net->pinned = nullptr;
+            CK(cudaMallocHost(&net->pinned, 2 * stage_bytes));
+            net->pinned_cap = stage_bytes;
+        }
+        for (auto& e : net->stage_ev)
+            if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        char* stage[2] = {reinterpret_cast<char*>(net->pinned), reinterpret_cast<char*>(net->pinned) + net->pinned_cap};
+        int buf = 0;
+        for (int64_t c0 = 0; c0 < npix; c0 += (int64_t)net->pinned_cap, buf ^= 1) {
+            const int64_t len = std::min<int64_t>((int64_t)net->pinned_cap, npix - c0);
+            CK(cudaEventSynchronize(net->stage_ev[buf]));
+            char* dst = stage[buf];
+            const int64_t parts = 16;
+#pragma omp parallel for schedule(static)
+            for (int64_t q = 0; q < parts; ++q) {
+                const int64_t a = len * q / parts, e = len * (q + 1) / parts;
+                memcpy(dst + a, pixels + c0 + a, e - a);
+            }
+            CK(cudaMemcpyAsync(dpix + c0, dst, len, cudaMemcpyHostToDevice, st));
+            CK(cudaEventRecord(net->stage_ev[buf], st));
+        }
+    }
     CK(cudaMemcpyAsync(dtaps, taps.data(), t * sizeof(int2), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(dw, w.data(), t * sizeof(double2), cudaMemcpyHostToDevice, st));
     b->h2d_bytes = npix + t * (int64_t)(sizeof(int2) + sizeof(double2));

@@ -1227,91 +1227,122 @@ __device__ __forceinline__ double two_tap(double xlo, double xhi, double wlo, do
 }
 
 // One block per image: pass 1 (t x side) into shared memory, pass 2 writes
-// the t*t threshold bits as 32-bit words and the image's entry count.
+// the t*t threshold bits as 32-bit words and the image's entry count.  The
+// taps and the 256 values k / 255 live in shared memory.  Pass 1: lane =
+// source column, warp = output row.  Pass 2: a warp owns one block of 32
+// output columns for good (taps in registers) and walks output rows; one
+// ballot forms each row's 32-bit word.  Needs t a multiple of 32 with
+// t / 32 dividing the warp count (t <= 256: the reference's target sides).
 __global__ void resize_bits_kernel(const uint8_t* __restrict__ pix, int64_t n, int side, int t,
                                    const int2* __restrict__ taps, const double2* __restrict__ w,
                                    uint32_t* __restrict__ bits, int64_t* __restrict__ count) {
     extern __shared__ __align__(16) unsigned char rsm[];
-    double* img = reinterpret_cast<double*>(rsm);  // [side][side]
-    double* tmp = img + side * side;                // [t][side]
+    double2* sw = reinterpret_cast<double2*>(rsm);         // [t]
+    double* lut = reinterpret_cast<double*>(sw + t);       // [256]: k / 255
+    int2* st = reinterpret_cast<int2*>(lut + 256);         // [t]
+    double* img = reinterpret_cast<double*>(st + t);       // [side][side]
+    double* tmp = img + side * side;                       // [t][side]
     __shared__ int s_cnt[32];
-    const int words = t * t / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int wpr = t / 32;  // words per output row
+    for (int i = threadIdx.x; i < t; i += blockDim.x) {
+        sw[i] = w[i];
+        st[i] = taps[i];
+    }
+    for (int k = threadIdx.x; k < 256; k += blockDim.x) lut[k] = __ddiv_rn((double)k, 255.0);
+    __syncthreads();
+    // pass-2 ownership: column block jb, rows i0, i0 + step, ...
+    const int jb = warp % wpr, i0 = warp / wpr, step = nw / wpr;
+    const int jc = jb * 32 + lane;
+    const int2 ctp = st[jc];
+    const double2 cw = sw[jc];
+    const bool two = ctp.y >= 0;
+    const int chi = max(ctp.y, 0);
     for (int64_t im = blockIdx.x; im < n; im += gridDim.x) {
         const uint8_t* P = pix + im * side * side;
-        for (int i = threadIdx.x; i < side * side; i += blockDim.x) img[i] = __ddiv_rn((double)P[i], 255.0);
+        for (int i = threadIdx.x; i < side * side; i += blockDim.x) img[i] = lut[P[i]];
         __syncthreads();
-        for (int e = threadIdx.x; e < t * side; e += blockDim.x) {
-            const int i = e / side, b = e % side;
-            const int2 tp = taps[i];
-            const double2 ww = w[i];
-            tmp[e] = two_tap(img[tp.x * side + b], img[max(tp.y, 0) * side + b], ww.x, ww.y, tp.y >= 0);
+        for (int i = warp; i < t; i += nw) {
+            const int2 tp = st[i];
+            const double2 ww = sw[i];
+            const double* lo = img + tp.x * side;
+            const double* hi = img + max(tp.y, 0) * side;
+            for (int b = lane; b < side; b += 32)
+                tmp[i * side + b] = two_tap(lo[b], hi[b], ww.x, ww.y, tp.y >= 0);
         }
         __syncthreads();
+        // the words of 32 consecutive rows are collected one per lane, then
+        // stored (and counted) by all lanes at once
         int c = 0;
-        for (int q = threadIdx.x; q < words; q += blockDim.x) {
-            const int i = (q * 32) / t, j0 = (q * 32) % t;
-            const double* row = tmp + i * side;
-            uint32_t v = 0u;
-#pragma unroll 4
-            for (int u = 0; u < 32; ++u) {
-                const int2 tp = taps[j0 + u];
-                const double2 ww = w[j0 + u];
-                const double x = two_tap(row[tp.x], row[max(tp.y, 0)], ww.x, ww.y, tp.y >= 0);
-                v |= (x >= 0.5 ? 1u : 0u) << u;
+        uint32_t* out = bits + im * (int64_t)(t * wpr) + jb;
+        const double* rowp = tmp + i0 * side;
+        const int rstep = step * side;
+        uint32_t mine = 0u;
+        int r = 0, ifirst = i0;
+        for (int i = i0; i < t; i += step, rowp += rstep) {
+            const double x = two_tap(rowp[ctp.x], rowp[chi], cw.x, cw.y, two);
+            const unsigned v = __ballot_sync(0xffffffffu, x >= 0.5);
+            mine = lane == r ? v : mine;
+            if (++r == 32 || i + step >= t) {
+                if (lane < r) {
+                    out[(ifirst + lane * step) * wpr] = mine;
+                    c += __popc(mine);
+                }
+                r = 0;
+                ifirst = i + step;
             }
-            bits[im * words + q] = v;
-            c += __popc(v);
         }
         for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-        if ((threadIdx.x & 31) == 0) s_cnt[threadIdx.x >> 5] = c;
+        if (lane == 0) s_cnt[warp] = c;
         __syncthreads();
         if (threadIdx.x == 0) {
             int64_t s = 0;
-            for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += s_cnt[k];
+            for (int k = 0; k < nw; ++k) s += s_cnt[k];
             count[im] = s;
         }
-        __syncthreads();
     }
 }
 
 // Threshold bits -> CSR columns (ascending), one block per image; cols are
 // uint16 when t*t <= 65536 else int32 (the engine's device batch layout).
+// Each warp owns a contiguous run of words: a popcount pass and a scan over
+// the warps give its first offset, then word by word (broadcast by shuffle)
+// the set lanes write their columns as one coalesced store.
 template <typename C>
 __global__ void bits_to_cols_kernel(const uint32_t* __restrict__ bits, int64_t n, int words,
                                     const int64_t* __restrict__ off, C* __restrict__ cols) {
-    __shared__ int s_warp[32];
-    __shared__ int64_t s_base;
+    __shared__ int64_t s_base[32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const unsigned below = (1u << lane) - 1u;
+    const int per = (words + nw - 1) / nw;
+    const int q0 = min(words, warp * per), q1 = min(words, q0 + per);
     for (int64_t im = blockIdx.x; im < n; im += gridDim.x) {
-        if (threadIdx.x == 0) s_base = off[im];
-        __syncthreads();
         const uint32_t* B = bits + im * words;
-        for (int q0 = 0; q0 < words; q0 += blockDim.x) {
-            const int q = q0 + threadIdx.x;
-            const uint32_t v = q < words ? B[q] : 0u;
-            const int c = __popc(v);
-            int x = c;  // inclusive scan over the block
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
+        int c = 0;
+        for (int q = q0 + lane; q < q1; q += 32) c += __popc(B[q]);
+        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) s_base[warp] = c;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int64_t acc = off[im];
+            for (int k = 0; k < nw; ++k) {
+                const int64_t x = s_base[k];
+                s_base[k] = acc;
+                acc += x;
             }
-            if (lane == 31) s_warp[warp] = x;
-            __syncthreads();
-            if (warp == 0) {
-                int s = lane < nw ? s_warp[lane] : 0;
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int y = __shfl_up_sync(0xffffffffu, s, o);
-                    if (lane >= o) s += y;
-                }
-                if (lane < nw) s_warp[lane] = s;
-            }
-            __syncthreads();
-            int64_t at = s_base + (warp ? s_warp[warp - 1] : 0) + x - c;
-            for (uint32_t m = v; m; m &= m - 1) cols[at++] = (C)(q * 32 + __ffs(m) - 1);
-            __syncthreads();
-            if (threadIdx.x == 0) s_base += s_warp[nw - 1];
-            __syncthreads();
         }
+        __syncthreads();
+        int64_t base = s_base[warp];
+        for (int qb = q0; qb < q1; qb += 32) {
+            const uint32_t mine = qb + lane < q1 ? B[qb + lane] : 0u;
+            const int m = min(32, q1 - qb);
+            for (int k = 0; k < m; ++k) {
+                const uint32_t v = __shfl_sync(0xffffffffu, mine, k);
+                if ((v >> lane) & 1u) cols[base + __popc(v & below)] = (C)((qb + k) * 32 + lane);
+                base += __popc(v);
+            }
+        }
+        __syncthreads();  // s_base is rewritten for the next image
     }
 }
 

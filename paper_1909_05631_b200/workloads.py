@@ -126,3 +126,27 @@ def layers_csr(w: Workload, first: int = 0, count: int | None = None, threads: i
 
     with ThreadPoolExecutor(max_workers=t) as pool:
         return list(pool.map(one, range(count)))
+
+
+def stroke_images(n: int, seed: int = IMAGE_SEED, side: int = 28) -> np.ndarray:
+    """Seeded MNIST-shaped stand-in corpus for the device ingest path: each
+    image holds 2-4 thick strokes with soft (anti-aliased) edges, so the
+    resampled values cross the 0.5 threshold at fractional positions.
+    uint8, shape (n, side, side)."""
+    rng = np.random.default_rng(seed)
+    yy, xx = np.mgrid[0:side, 0:side].astype(np.float32)
+    img = np.zeros((n, side, side), np.float32)
+    for s in range(4):
+        a = rng.uniform(4, side - 4, size=(n, 2)).astype(np.float32)
+        b = rng.uniform(4, side - 4, size=(n, 2)).astype(np.float32)
+        width = rng.uniform(1.0, 2.2, size=n).astype(np.float32)
+        on = rng.random(n) < (1.0 if s < 2 else 0.5)
+        d = b - a
+        L2 = np.maximum((d ** 2).sum(axis=1), 1e-3)
+        px = xx[None] - a[:, 0, None, None]
+        py = yy[None] - a[:, 1, None, None]
+        t = np.clip((px * d[:, 0, None, None] + py * d[:, 1, None, None]) / L2[:, None, None], 0, 1)
+        dist = np.hypot(px - t * d[:, 0, None, None], py - t * d[:, 1, None, None])
+        ink = np.clip(width[:, None, None] + 0.5 - dist, 0.0, 1.0) * on[:, None, None]
+        img = np.maximum(img, ink)
+    return np.rint(img * 255.0).astype(np.uint8)
