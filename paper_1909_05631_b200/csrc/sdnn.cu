@@ -949,12 +949,25 @@ int images_upload(sdnn_net* net, int64_t n, int side, const uint8_t* pixels, int
     uint32_t* bits = nullptr;
     int64_t* cnt = nullptr;
     const int64_t npix = n * side * side;
+    // scratch freed on every exit path (stream-ordered)
+    struct Scratch {
+        cudaStream_t st;
+        std::vector<void*> p;
+        ~Scratch() {
+            for (void* q : p) cudaFreeAsync(q, st);
+        }
+    } scratch{st, {}};
+    auto alloc = [&](void** q, size_t bytes) {
+        cudaError_t e = cudaMallocAsync(q, bytes, st);
+        if (e == cudaSuccess) scratch.p.push_back(*q);
+        return e;
+    };
     CK(cudaMallocAsync(reinterpret_cast<void**>(&b->off), (n + 1) * sizeof(int64_t), st));
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&dpix), std::max<int64_t>(npix, 1), st));
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&dtaps), t * sizeof(int2), st));
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&dw), t * sizeof(double2), st));
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&bits), std::max<int64_t>(n * words, 1) * 4, st));
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&cnt), std::max<int64_t>(n, 1) * 8, st));
+    CK(alloc(reinterpret_cast<void**>(&dpix), std::max<int64_t>(npix, 1)));
+    CK(alloc(reinterpret_cast<void**>(&dtaps), t * sizeof(int2)));
+    CK(alloc(reinterpret_cast<void**>(&dw), t * sizeof(double2)));
+    CK(alloc(reinterpret_cast<void**>(&bits), std::max<int64_t>(n * words, 1) * 4));
+    CK(alloc(reinterpret_cast<void**>(&cnt), std::max<int64_t>(n, 1) * 8));
     if (npix) {  // pageable pixels -> pinned staging (host threads) -> device, chunk by chunk
         const int64_t chunk = 16 << 20;
         const size_t stage_bytes = (size_t)std::min<int64_t>(chunk, npix);
@@ -1016,11 +1029,6 @@ int images_upload(sdnn_net* net, int64_t n, int side, const uint8_t* pixels, int
                                                                reinterpret_cast<int32_t*>(b->cols));
         CK(cudaGetLastError());
     }
-    CK(cudaFreeAsync(dpix, st));
-    CK(cudaFreeAsync(dtaps, st));
-    CK(cudaFreeAsync(dw, st));
-    CK(cudaFreeAsync(bits, st));
-    CK(cudaFreeAsync(cnt, st));
     CK(cudaStreamSynchronize(st));
     return SDNN_OK;
 }
