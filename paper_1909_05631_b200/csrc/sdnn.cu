@@ -667,6 +667,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     const int grid = net->sm_count * occ;
     void* args[] = {(void*)&a};
     CK(cudaEventRecord(net->ev0, net->stream));
+    bool quad = false;  // layer 1 over quad bit-lines (binary Y0, float)
     if (n_tiles) {
         // lines densify does not touch stay {mask 0}: zero the meta first
         CK(cudaMemsetAsync(a.meta[0], 0, (size_t)n_tiles * ld * sizeof(uint2), net->stream));
@@ -675,6 +676,9 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
         const bool bin = batch->vals == nullptr && env_int("SDNN_BIN", 1) != 0;
         a.bin_in = bin ? 1 : 0;
         if (bin) {  // binary Y0: bit-line tiles
+            quad = sizeof(T) == 4 && env_int("SDNN_QUAD", 1) != 0;
+            if (quad)  // quad lines of dead neurons / missing tiles must read as zero
+                CK(cudaMemsetAsync(a.slab[0], 0, (size_t)((n_tiles + 3) / 4) * ld * 128, net->stream));
             const int kcb = 1024;
             const int span = (int)(((n_in + spans - 1) / spans + kcb - 1) / kcb * kcb);
             const int64_t blocks = n_tiles * ((n_in + span - 1) / span);
@@ -684,7 +688,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
                                     (int)bsmem));
             densify_bin_kernel<T><<<dgrid, kDensifyThreads, bsmem, net->stream>>>(
                 batch->off, batch->cols, batch->col_bytes, net->rowid, (int)n_in, (int)ld, (int)n_tiles, kcb, span,
-                a.slab[0], a.meta[0], heap, net->alive, tile_count);
+                a.slab[0], a.meta[0], heap, net->alive, tile_count, quad ? 1 : 0);
         } else {
             const int span = (int)(((n_in + spans - 1) / spans + kc - 1) / kc * kc);
             const int64_t blocks = n_tiles * ((n_in + span - 1) / span);
@@ -697,7 +701,16 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
         res->launches += 1;
     }
     CK(cudaEventRecord(net->ev_d, net->stream));
-    if (a.bin_in) {  // layer 1 over bit-line tiles: its own launch
+    if (a.bin_in && quad) {  // layer 1 over quad bit-lines (float): its own launch
+        const void* qfn = (const void*)bin_quad_kernel;
+        int qocc = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&qocc, qfn, kThreads, 0));
+        bin_quad_kernel<<<net->sm_count * std::max(qocc, 1), kThreads, 0, net->stream>>>(
+            *reinterpret_cast<NetArgs<float>*>(&a));
+        CK(cudaGetLastError());
+        res->launches += 1;
+        a.first_l = 1;
+    } else if (a.bin_in) {  // layer 1 over bit-line tiles: its own launch
         const void* bfn = (const void*)bin_layer_kernel<T>;
         CK(cudaFuncSetAttribute(bfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int bocc = 0;

@@ -459,7 +459,8 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_bin_kernel(const int6
                                                                       const int32_t* __restrict__ rowid, int n_in,
                                                                       int ld, int n_tiles, int kc, int span,
                                                                       T* slab0, uint2* meta0, uint32_t* heap0,
-                                                                      uint32_t* alive0, int32_t* tile_count0) {
+                                                                      uint32_t* alive0, int32_t* tile_count0,
+                                                                      int quad) {
     extern __shared__ __align__(16) unsigned char dsm[];
     constexpr int TR = tile_rows<T>(), AW = alive_words<T>(), W = TR / 32;  // words per bit-line
     constexpr int NW = kDensifyThreads / 32, RW = TR / NW;
@@ -543,7 +544,13 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_bin_kernel(const int6
                     stage[at] = 0u;
                     any |= wv[q];
                 }
-                if (any) {
+                if (any && quad) {  // quad layout: tile t's 32 bytes of quad line (t / 4, k)
+                    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<char*>(slab0) +
+                                                          ((size_t)(t >> 2) * ld + (k0 + k)) * 128 + (t & 3) * 32);
+                    dst[0] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                    dst[1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
+                    gm[k0 + k] = make_uint2(0xFFFFFFFFu, (unsigned)(k0 + k));
+                } else if (any) {
                     const unsigned base = atomicAdd(&heap0[t], 1u);
                     uint4* dst = reinterpret_cast<uint4*>(s0 + (size_t)base * 32);
                     dst[0] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
@@ -1057,6 +1064,206 @@ __global__ void __launch_bounds__(kThreads, bin_occ<T>()) bin_layer_kernel(NetAr
         layer_pass<T, bin_gb<T>(), true, false, 2>(a, 0, reinterpret_cast<int32_t*>(smem), sh);
     else
         layer_pass<T, bin_gb<T>(), true, false>(a, 0, reinterpret_cast<int32_t*>(smem), sh);
+}
+
+// ------------------------------------- layer 1 over quad bit-lines (float)
+// Binary Y0 with four consecutive tiles interleaved: the 128-byte quad line
+// (quad q, neuron k) holds the 32-byte bit-lines of tiles 4q .. 4q+3 one
+// after the other (densify_bin_kernel, quad mode), so lane l reads ONE
+// 32-bit word per slot -- 32 rows (32*(l%8) .. +31) of tile 4q + l/8 -- and
+// a slot list, its loads and its loop serve 1,024 rows instead of 256.  The
+// per-column epilogue writes each lane's four float sectors into its tile's
+// line; a tile's kept-sector mask is assembled from its eight lanes'
+// nibbles by three shuffles.  Quad lines of dead tiles / neurons are zero
+// (the quad slab is cleared before densify), and a zero line adds nothing.
+#ifndef SDNN_QUAD_GB
+#define SDNN_QUAD_GB 2
+#endif
+#ifndef SDNN_QUAD_OCC
+#define SDNN_QUAD_OCC 3  // 80 registers, no spills (2: 6.0 ms, 4: spills, 5.3 ms)
+#endif
+constexpr int kQuadLine = 128;  // bytes per (quad, neuron) line
+
+template <int GB>
+__device__ __forceinline__ void bin_quad_item(const NetArgs<float>& a, const LayerDesc<float>& L, int q,
+                                              int j0, int j1, uint2* wlist) {
+    constexpr int AW = alive_words<float>();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int T = lane >> 3, sub = lane & 7;  // this lane's tile within the quad, its row group
+    const unsigned below = (1u << lane) - 1u;
+    const int t0 = q * 4, ntq = min(4, a.n_tiles - t0);
+    const int t = t0 + min(T, ntq - 1);
+    const bool tile_ok = T < ntq;
+    const unsigned* inq = reinterpret_cast<const unsigned*>(reinterpret_cast<const char*>(a.slab[0]) +
+                                                            (size_t)q * a.ld * kQuadLine) + lane;
+    asm("mov.b64 %0, %0;" : "+l"(inq));
+    const size_t tile_lines = (size_t)t * a.ld;
+    char* out = reinterpret_cast<char*>(a.slab[1]) + tile_lines * kLineBytes;
+    uint2* ometa = a.meta[1] + tile_lines;
+    const uint2* m0p = a.meta[0] + (size_t)t0 * a.ld;  // liveness: any tile of the quad
+    const int jw = j0 + warp;
+    if (jw >= j1) return;
+    const int nb = L.wp / 32;
+    const int n_cols = (j1 - jw + kWarps - 1) / kWarps;
+    const int total = n_cols * nb;
+    if (total == 0) {
+        for (int j = jw; j < j1; j += kWarps)
+            if (sub == 0 && tile_ok) ometa[j] = make_uint2(0u, 0u);
+        return;
+    }
+    size_t po = (size_t)jw * L.wp + lane;
+    int pb = 0;
+    const size_t col_skip = (size_t)(kWarps - 1) * L.wp;
+    auto advance = [&]() {
+        po += 32;
+        if (++pb == nb) {
+            pb = 0;
+            po += col_skip;
+        }
+    };
+    auto quad_live = [&](int k) -> bool {
+        if (k < 0) return false;
+        unsigned any = 0u;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (u < ntq) any |= m0p[(size_t)u * a.ld + k].x;
+        return any != 0u;
+    };
+    const uint64_t wpol = policy_evict_last();
+    int k0 = ld_w(L.idx + po, wpol);
+    float w0 = ld_w(L.val + po, wpol);
+    advance();
+    int k1 = -1, k2 = -1;
+    float w1 = 0.f, w2 = 0.f;
+    if (total > 1) {
+        k1 = ld_w(L.idx + po, wpol);
+        w1 = ld_w(L.val + po, wpol);
+        advance();
+    }
+    bool l0 = quad_live(k0);
+    float acc[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) acc[c] = 0.f;
+    unsigned alive32 = 0u;
+    int cj = jw, cb = 0;
+    for (int b = 0; b < total; ++b) {
+        if (b + 2 < total) {
+            k2 = ld_w(L.idx + po, wpol);
+            w2 = ld_w(L.val + po, wpol);
+            advance();
+        }
+        const bool l1 = (b + 1 < total) ? quad_live(k1) : false;
+        const unsigned live = __ballot_sync(0xffffffffu, l0);
+        const int n = __popc(live);
+        const int npad = (n + GB - 1) / GB * GB;
+        {
+            uint2 e;
+            int at;
+            if (l0) {
+                e = make_uint2((unsigned)k0 * (kQuadLine / 4), __float_as_uint(w0));
+                at = __popc(live & below);
+            } else {  // padding: word 0 of line 0, weight 0 (adds +0)
+                e = make_uint2(0u, 0u);
+                at = n + __popc(~live & below);
+            }
+            if (at < npad) wlist[at] = e;
+        }
+        __syncwarp();
+        auto issue = [&](unsigned (&wd)[GB], float (&wv)[GB], int i0) {
+#pragma unroll
+            for (int u = 0; u < GB; ++u) {
+                const uint2 e = wlist[i0 + u];
+                wd[u] = __ldg(inq + e.x);
+                wv[u] = __uint_as_float(e.y);
+            }
+        };
+        auto consume = [&](const unsigned (&wd)[GB], const float (&wv)[GB]) {
+#pragma unroll
+            for (int u = 0; u < GB; ++u)
+#pragma unroll
+                for (int c = 0; c < 32; ++c)
+                    if ((wd[u] >> c) & 1u) acc[c] = __fadd_rn(acc[c], wv[u]);
+        };
+        unsigned d0[GB], d1[GB];
+        float v0[GB], v1[GB];
+        if (npad) issue(d0, v0, 0);
+        for (int i0 = 0; i0 < npad; i0 += 2 * GB) {
+            if (i0 + GB < npad) issue(d1, v1, i0 + GB);
+            consume(d0, v0);
+            if (i0 + GB >= npad) break;
+            if (i0 + 2 * GB < npad) issue(d0, v0, i0 + 2 * GB);
+            consume(d1, v1);
+        }
+        __syncwarp();
+        if (++cb == nb) {  // column complete: four sectors per lane
+            cb = 0;
+            unsigned bits[4];
+            float v[4][8];
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+                bits[g] = 0u;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    bool keep;
+                    if (a.epilogue) {
+                        v[g][c] = bias_relu_clamp_keep(acc[g * 8 + c], L.bias, a.ymax, keep);
+                    } else {
+                        v[g][c] = acc[g * 8 + c];
+                        keep = v[g][c] != 0.f;
+                    }
+                    bits[g] |= keep ? (1u << c) : 0u;
+                    acc[g * 8 + c] = 0.f;
+                }
+            }
+            // the tile's sector mask: lane sub contributes bits 4*sub .. 4*sub+3
+            unsigned nib = (bits[0] ? 1u : 0u) | (bits[1] ? 2u : 0u) | (bits[2] ? 4u : 0u) | (bits[3] ? 8u : 0u);
+            unsigned m = nib << (4 * sub);
+            m |= __shfl_xor_sync(0xffffffffu, m, 1);
+            m |= __shfl_xor_sync(0xffffffffu, m, 2);
+            m |= __shfl_xor_sync(0xffffffffu, m, 4);
+            const unsigned hb = (unsigned)cj * 32u;
+            if (tile_ok) {
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    const unsigned lp = (unsigned)(sub * 4 + g);
+                    if (bits[g]) st32(out + (size_t)(hb + __popc(m & ((1u << lp) - 1u))) * 32, v[g]);
+                }
+                if (sub == 0) ometa[cj] = make_uint2(m, hb);
+            }
+            alive32 |= bits[0] | (bits[1] << 8) | (bits[2] << 16) | (bits[3] << 24);
+            cj += kWarps;
+        }
+        k0 = k1;
+        w0 = w1;
+        l0 = l1;
+        k1 = k2;
+        w1 = w2;
+    }
+    // live rows: word `sub` of tile t is exactly this lane's 32 rows
+    uint32_t* aw = a.alive + ((size_t)1 * a.n_tiles + t) * AW;
+    if (tile_ok && alive32) atomicOr(&aw[sub], alive32);
+    const unsigned any = __ballot_sync(0xffffffffu, tile_ok && alive32 != 0u);
+    if (sub == 0 && ((any >> (8 * T)) & 0xffu) && atomicOr(&aw[AW - 1], 1u) == 0u) atomicAdd(&a.tile_count[1], 1);
+}
+
+__global__ void __launch_bounds__(kThreads, SDNN_QUAD_OCC) bin_quad_kernel(NetArgs<float> a) {
+    __shared__ uint2 lists[kWarps][32];
+    __shared__ long long s_item;
+    if (a.stamps && blockIdx.x == 0 && threadIdx.x == 0) a.stamps[0] = globaltimer();
+    if (__ldcg(&a.tile_count[0]) == 0) return;
+    const LayerDesc<float> L = a.layers[0];
+    const int nblk = (a.n_out + a.jb - 1) / a.jb;
+    const long long items = (long long)((a.n_tiles + 3) / 4) * nblk;
+    for (;;) {
+        if (threadIdx.x == 0) s_item = (long long)atomicAdd(&a.work[0], 1u);
+        __syncthreads();
+        const long long it = s_item;
+        __syncthreads();
+        if (it >= items) break;
+        const int q = (int)(it / nblk), bb = (int)(it % nblk);
+        const int j0 = bb * a.jb, j1 = min(a.n_out, j0 + a.jb);
+        bin_quad_item<SDNN_QUAD_GB>(a, L, q, j0, j1, lists[threadIdx.x >> 5]);
+    }
 }
 
 // All remaining layers (from a.first_l) in one cooperative launch with a
