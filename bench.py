@@ -453,6 +453,9 @@ def companions(args, net_cls):
         b = net.upload_csr(w.batch, off, cols, vals)
         net.run(b, w.ymax)
         r = net.run(b, w.ymax)
+        net.set_compaction(0)  # the same run without live-row compaction, for comparison
+        r0 = net.run(b, w.ymax)
+        net.set_compaction(10)
         net.set_layer_timing(True)
         p = net.run(b, w.ymax)
         elem = 8 if args.dtype == "f64" else 4
@@ -465,6 +468,8 @@ def companions(args, net_cls):
             "ms_per_step": r.device_ms,
             "live_rows_last_layer": int(p.live_rows[-2]),
             "categories": int(r.categories.size),
+            "row_compactions": int(r.compactions),
+            "ms_per_step_without_compaction": r0.device_ms,
             "steady_layer_ms": float(p.layer_ms[mid]),
             "steady_layer_gbs": lb[mid] / (p.layer_ms[mid] * 1e-3) / 1e9 if p.layer_ms[mid] > 0 else 0,
             "steady_layer_frac": (lb[mid] / (p.layer_ms[mid] * 1e-3) / 1e9) / peak if p.layer_ms[mid] > 0 else 0,

@@ -175,6 +175,14 @@ int sdnn_result_layer_ms(const sdnn_result *r, double *ms);
 int sdnn_result_stage_ms(const sdnn_result *r, double *ms);
 /* Kernel launches the run issued (evidence for bench gpu_launches). */
 int sdnn_result_launches(const sdnn_result *r, int64_t *n);
+/* Live-row compaction: before a layer, the live rows
+ * are repacked densely into tiles when that frees at least `pct` % of the
+ * live tiles (default 10; <= 0 never; the SDNN_COMPACT environment variable
+ * overrides).  Results are bit-identical either way.  No reference
+ * counterpart: the reference's CSR rows carry no dead-row cost. */
+int sdnn_net_set_compaction(sdnn_net *net, int pct);
+/* Row compactions the run performed (summed over waves / segments). */
+int sdnn_result_compactions(const sdnn_result *r, int64_t *n);
 /* Final Y as canonical CSR (ascending columns, no zeros) widened to
  * float64: query nnz first, then fill caller buffers. */
 int sdnn_result_y_nnz(sdnn_result *r, int64_t *nnz);

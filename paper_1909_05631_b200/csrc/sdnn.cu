@@ -126,6 +126,11 @@ struct sdnn_net {
     int64_t acap = 0;
     int32_t* rowid_buf = nullptr;  // per-run scratch below: grown, never freed per run
     int64_t idcap = 0;
+    int32_t* rowid_alt = nullptr;  // the row-id map after an odd number of row compactions
+    int64_t idcap2 = 0;
+    uint32_t* alive_c = nullptr;   // row bitmaps of repacked tiles
+    int64_t accap = 0;
+    int* n_compact = nullptr;
     int32_t* tile_count = nullptr;
     int64_t* live_rows = nullptr;
     unsigned long long* stamps = nullptr;
@@ -142,6 +147,7 @@ struct sdnn_net {
     size_t pinned_cap = 0;
     cudaEvent_t stage_ev[2] = {nullptr, nullptr};
     int layer_timing = 0;
+    int compact_pct = 10;  // live-row compaction threshold (% of live tiles freed)
     // weight-ingest scratch (CSR -> ELL on the device), grown on demand
     void* ing_pinned = nullptr;
     size_t ing_pinned_cap = 0;
@@ -171,6 +177,7 @@ struct sdnn_result {
     double stage_ms[3] = {0, 0, 0};  // densify, first (bit-line) layer launch, persistent layer launch
     int64_t h2d_bytes = 0;  // host -> device bytes of the call's uploads (end-to-end calls)
     int64_t segments = 0;   // row segments of a streamed call
+    int64_t compactions = 0;  // live-row compactions in the run
     bool have_y = false;
     std::vector<int64_t> off, cols;
     std::vector<double> vals;
@@ -591,6 +598,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     const int64_t n_tiles = (n_live + TR - 1) / TR;
     if (int rc = ensure_tiles(net, n_tiles, ld)) return rc;
     if (int rc = grow(net->rowid_buf, net->idcap, std::max<int64_t>(n_tiles * TR, 1), 4)) return rc;
+    if (int rc = grow(net->rowid_alt, net->idcap2, std::max<int64_t>(n_tiles * TR, 1), 4)) return rc;
     net->rowid = net->rowid_buf;
     CK(cudaMemsetAsync(net->rowid, 0xff, std::max<int64_t>(n_tiles * TR, 1) * 4, net->stream));
     if (n_live) CK(cudaMemcpyAsync(net->rowid, net->rowlist, n_live * 4, cudaMemcpyDeviceToDevice, net->stream));
@@ -603,7 +611,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
         if (int rc = grow(net->tile_count, c1, nl + 1, 4)) return rc;
         if (int rc = grow(net->live_rows, c2, nl + 1, 8)) return rc;
         if (int rc = grow(net->stamps, c3, nl + 1, 8)) return rc;
-        if (int rc = grow(net->work, c4, nl + 1, 4)) return rc;
+        if (int rc = grow(net->work, c4, 2 * (nl + 1), 4)) return rc;  // layers, then compactions
         net->lcap = nl + 1;
     }
     int32_t* tile_count = net->tile_count;
@@ -622,7 +630,10 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     uint32_t* heap = net->heap;
     CK(cudaMemsetAsync(heap, 0, (nl + 1) * tiles1 * 4, net->stream));
     unsigned* work = net->work;
-    CK(cudaMemsetAsync(work, 0, std::max<int64_t>(nl, 1) * 4, net->stream));
+    CK(cudaMemsetAsync(work, 0, 2 * std::max<int64_t>(nl, 1) * 4, net->stream));
+    if (int rc = grow(net->alive_c, net->accap, tiles1 * AW, 4)) return rc;
+    if (!net->n_compact) CK(cudaMalloc(&net->n_compact, 4));
+    CK(cudaMemsetAsync(net->n_compact, 0, 4, net->stream));
 
     NetArgs<T> a{};
     a.n_in = (int)n_in;
@@ -644,6 +655,12 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     a.bar = net->bar;
     a.work = work;
     a.stamps = net->layer_timing ? stamps : nullptr;
+    a.rowid[0] = net->rowid_buf;
+    a.rowid[1] = net->rowid_alt;
+    a.alive_c = net->alive_c;
+    a.n_compact = net->n_compact;
+    // live-row compaction: repack once that % of the live tiles would be freed
+    a.compact_pct = env_int("SDNN_COMPACT", net->compact_pct);
     a.jb = env_int("SDNN_JB", net->jb);
     const int kc = std::min(1024, env_int("SDNN_DENSIFY_KC", 96));  // input neurons per staging chunk
     const size_t dsmem = (size_t)kc * kLineBytes;
@@ -658,7 +675,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
 #endif
     const void* fn = zfill ? (const void*)net_kernel<T, SDNN_NET_GB, true>
                            : (const void*)net_kernel<T, SDNN_NET_GB, false>;
-    const size_t smem = (size_t)tiles1 * 4;
+    const size_t smem = (size_t)(2 * tiles1 + 1) * 4;  // live-tile list + row prefix
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem));
@@ -733,12 +750,18 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     std::vector<unsigned long long> st(nl + 1);
     std::vector<uint32_t> alive_last(tiles1 * AW);
     std::vector<int32_t> rowid(n_tiles * TR);
+    int n_compact = 0;
+    CK(cudaMemcpyAsync(&n_compact, net->n_compact, 4, cudaMemcpyDeviceToHost, net->stream));
     CK(cudaMemcpyAsync(lr.data(), live, (nl + 1) * 8, cudaMemcpyDeviceToHost, net->stream));
     CK(cudaMemcpyAsync(st.data(), stamps, (nl + 1) * 8, cudaMemcpyDeviceToHost, net->stream));
     CK(cudaMemcpyAsync(alive_last.data(), net->alive + nl * tiles1 * AW, tiles1 * AW * 4, cudaMemcpyDeviceToHost,
                        net->stream));
-    if (n_tiles) CK(cudaMemcpyAsync(rowid.data(), net->rowid, n_tiles * TR * 4, cudaMemcpyDeviceToHost, net->stream));
     CK(cudaStreamSynchronize(net->stream));
+    // an odd number of compactions leaves the row-id map in the other buffer
+    // and the final slab in the other parity
+    if (n_compact & 1) net->rowid = net->rowid_alt;
+    res->compactions += n_compact;
+    if (n_tiles) CK(cudaMemcpy(rowid.data(), net->rowid, n_tiles * TR * 4, cudaMemcpyDeviceToHost));
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, net->ev0, net->ev1));
     dev_ms += ms;
@@ -760,7 +783,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
             if ((alive_last[t * AW + r / 32] >> (r % 32)) & 1u) final_rows.push_back(rowid[t * TR + r]);
     if (want_y && r0 == 0 && r1 == batch->n_rows && env_int("SDNN_HOST_Y", 0) == 0) {
         // the whole batch in one wave: Y goes straight into a device CSR
-        const int last = (int)(nl & 1);
+        const int last = (int)((nl + n_compact) & 1);
         res->n_rows = batch->n_rows;
         int rc = extract_device<T>(net, reinterpret_cast<const T*>(net->slab[last]), net->meta[last], (int)ld,
                                    (int)n_out, n_tiles, net->alive + nl * tiles1 * AW, batch->n_rows, res);
@@ -769,7 +792,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     }
     if (want_y) {
         Piece p;
-        const int last = (int)(nl & 1);  // layer nl-1 wrote buffer nl & 1
+        const int last = (int)((nl + n_compact) & 1);  // layer nl-1 wrote buffer (nl + flips) & 1
         if (int rc = extract<T>(net, reinterpret_cast<const T*>(net->slab[last]), net->meta[last], (int)ld,
                                 (int)n_out, n_tiles, alive_last, rowid, p))
             return rc;
@@ -1231,6 +1254,7 @@ void merge_part(sdnn_result* res, const sdnn_result& part, int64_t r0, int want_
     for (size_t l = 0; l < part.live.size(); ++l) res->live[l] += part.live[l];
     res->dev_ms += part.dev_ms;
     res->launches += part.launches;
+    res->compactions += part.compactions;
     for (int k = 0; k < 3; ++k) res->stage_ms[k] += part.stage_ms[k];
     for (size_t l = 0; l < part.layer_ms.size() && l < res->layer_ms.size(); ++l) res->layer_ms[l] += part.layer_ms[l];
     if (want_y) {
@@ -1406,6 +1430,9 @@ void sdnn_net_destroy(sdnn_net* net) {
     }
     cudaFree(net->zero);
     cudaFree(net->rowid_buf);
+    cudaFree(net->rowid_alt);
+    cudaFree(net->alive_c);
+    cudaFree(net->n_compact);
     cudaFree(net->rowlist);
     cudaFree(net->live_rows);
     cudaFree(net->stamps);
@@ -1786,6 +1813,18 @@ int sdnn_result_live_rows(const sdnn_result* r, int64_t* live) {
 int sdnn_net_set_layer_timing(sdnn_net* net, int on) {
     if (!net) return fail(SDNN_ERR_PARAMETER, "null argument");
     net->layer_timing = on;
+    return SDNN_OK;
+}
+
+int sdnn_net_set_compaction(sdnn_net* net, int pct) {
+    if (!net) return fail(SDNN_ERR_PARAMETER, "null argument");
+    net->compact_pct = pct;
+    return SDNN_OK;
+}
+
+int sdnn_result_compactions(const sdnn_result* r, int64_t* n) {
+    if (!r || !n) return fail(SDNN_ERR_PARAMETER, "null argument");
+    *n = r->compactions;
     return SDNN_OK;
 }
 

@@ -241,6 +241,12 @@ struct NetArgs {
     int jb;               // outputs per work item
     int bin_in;           // layer-0 input is bit-lines (binary Y0)
     int first_l;          // first layer net_kernel runs (1 after bin_layer_kernel)
+    // live-row compaction between layers (net_kernel)
+    int32_t* rowid[2];    // [n_tiles * TR] tile position -> batch row (-1: none); compaction g reads
+                          // rowid[g & 1] and writes rowid[(g + 1) & 1]
+    uint32_t* alive_c;    // [n_tiles][alive_words] row bitmap of the repacked tiles
+    int compact_pct;      // repack when >= this % of the live tiles would be freed (<= 0: never)
+    int* n_compact;       // compactions done (written by block 0 at the end)
 };
 
 constexpr int kThreads = 256;
@@ -583,16 +589,16 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_bin_kernel(const int6
 // lane's weight is 0 instead, y*0 + acc == acc.  The host picks ZFILL unless
 // every value the kernel can read is finite (Y0 finite and ymax finite).
 template <typename T, int GB, bool BIN, bool ZFILL>
-__device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<T>& L, int l, int t,
+__device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<T>& L, int l, bool odd, int t,
                                            int j0, int j1, SlotEntry<T>* wlist) {
     using A = Arith<T>;
     constexpr int RPL = rows_per_lane<T>(), AW = alive_words<T>();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lbit = 1u << lane;
     const size_t tile_lines = (size_t)t * a.ld;
-    // select, not index: a runtime index into the parameter struct would
-    // force a local-memory copy of it
-    const bool odd = l & 1;
+    // odd: the layer's input is in slab[1] (layer parity, flipped by each
+    // row compaction).  Select, not index: a runtime index into the
+    // parameter struct would force a local-memory copy of it
     const char* in = reinterpret_cast<const char*>(odd ? a.slab[1] : a.slab[0]) + tile_lines * kLineBytes;
     // one opaque 64-bit base: sector addresses are then a single wide
     // multiply-add (the compiler would otherwise re-add a uniform part)
@@ -972,6 +978,8 @@ __device__ __forceinline__ void bin_item2(const NetArgs<float>& a, const LayerDe
 template <typename T>
 struct LayerShared {
     SlotEntry<T> list[kWarps][32];
+    int src[tile_rows<T>()];  // row compaction: source (tile * TR + row) of each new row
+    int scan_c[2 * kWarps + 2];
     int count;
     int scan[kWarps + 1];
     long long item;
@@ -981,10 +989,11 @@ struct LayerShared {
 // layer's alive flags, then take (tile, output block) items in order from the
 // layer's counter until none are left.
 template <typename T, int GB, bool BIN, bool ZFILL, int TP = 1>
-__device__ __forceinline__ void layer_pass(const NetArgs<T>& a, int l, int32_t* tiles, LayerShared<T>& sh) {
+__device__ __forceinline__ void layer_pass(const NetArgs<T>& a, int l, int32_t* tiles, LayerShared<T>& sh,
+                                           bool odd = false, const uint32_t* alive_in = nullptr) {
     constexpr int AW = alive_words<T>();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t* alive_in = a.alive + (size_t)l * a.n_tiles * AW;
+    if (!alive_in) alive_in = a.alive + (size_t)l * a.n_tiles * AW;
     if (tid == 0) sh.count = 0;
     __syncthreads();
     for (int base = 0; base < a.n_tiles; base += kThreads) {
@@ -1028,7 +1037,7 @@ __device__ __forceinline__ void layer_pass(const NetArgs<T>& a, int l, int32_t* 
             bin_item2<GB>(a, L, tiles[ti], ti + 1 < count ? tiles[ti + 1] : -1, j0, j1,
                           reinterpret_cast<BinEntry2*>(sh.list[warp]));
         } else {
-            layer_item<T, GB, BIN, ZFILL>(a, L, l, tiles[ti], j0, j1, sh.list[warp]);
+            layer_item<T, GB, BIN, ZFILL>(a, L, l, odd, tiles[ti], j0, j1, sh.list[warp]);
         }
     }
 }
@@ -1266,6 +1275,157 @@ __global__ void __launch_bounds__(kThreads, SDNN_QUAD_OCC) bin_quad_kernel(NetAr
     }
 }
 
+// ------------------------------------------------ live-row compaction
+// Rows die independently, so after a few layers every live tile holds some
+// dead rows that still cost a full line gather per slot.  Before a layer,
+// every CTA scans the layer's live-row bitmaps (warp ballot + block prefix
+// scan over the tiles' row counts, redundantly per CTA: no extra barrier);
+// when packing the live rows densely would free at least compact_pct % of
+// the live tiles, the rows are repacked in ascending order into tiles
+// 0 .. ceil(live / TR) - 1 of the other slab (a row's values move, nothing
+// is recomputed: bit-identical), the row-id map follows, and the layer reads
+// the repacked slab.  All CTAs take the same decision from the same data, so
+// the slab parity flips in a register.
+
+// pre[t] = live rows in tiles < t (pre[n_tiles] = total), live tiles count.
+template <typename T>
+__device__ __forceinline__ void row_prefix(const uint32_t* alive_l, int n_tiles, int* pre, int* s_scan,
+                                           int& total, int& live_tiles) {
+    constexpr int AW = alive_words<T>();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int run = 0, lt = 0;
+    for (int base = 0; base < n_tiles; base += kThreads) {
+        const int t = base + tid;
+        int c = 0;
+        if (t < n_tiles) {
+            const uint32_t* w = alive_l + (size_t)t * AW;
+            if (__ldcg(&w[AW - 1]))
+#pragma unroll
+                for (int q = 0; q < AW - 1; ++q) c += __popc(__ldcg(&w[q]));
+        }
+        // inclusive warp scan of the counts, then across warps
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const unsigned lv = __ballot_sync(0xffffffffu, c != 0);
+        if (lane == 31) s_scan[warp] = incl;
+        if (lane == 0) s_scan[kWarps + 1 + warp] = __popc(lv);
+        __syncthreads();
+        int wbase = run;
+        for (int w = 0; w < warp; ++w) wbase += s_scan[w];
+        if (t < n_tiles) pre[t] = wbase + incl - c;
+        int add = 0, addt = 0;
+        for (int w = 0; w < kWarps; ++w) {
+            add += s_scan[w];
+            addt += s_scan[kWarps + 1 + w];
+        }
+        run += add;
+        lt += addt;
+        __syncthreads();
+    }
+    if (tid == 0) pre[n_tiles] = run;
+    __syncthreads();
+    total = run;
+    live_tiles = lt;
+}
+
+// Repack the live rows of layer l's input (slab parity `odd`) into the other
+// slab.  Items (new tile, block of jb lines) from the counter work[L + l];
+// warp per line, lane l its RPL new rows, each read from its old sector.
+template <typename T>
+__device__ __forceinline__ void compact_pass(const NetArgs<T>& a, int l, bool odd, int gen, const int* pre, int total,
+                             LayerShared<T>& sh) {
+    constexpr int RPL = rows_per_lane<T>(), TR = tile_rows<T>(), AW = alive_words<T>();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t* alive_l = a.alive + (size_t)l * a.n_tiles * AW;
+    const int32_t* rid_in = (gen & 1) ? a.rowid[1] : a.rowid[0];
+    int32_t* rid_out = (gen & 1) ? a.rowid[0] : a.rowid[1];
+    const T* in = odd ? a.slab[1] : a.slab[0];
+    T* out = odd ? a.slab[0] : a.slab[1];
+    const uint2* imeta = odd ? a.meta[1] : a.meta[0];
+    uint2* ometa = odd ? a.meta[0] : a.meta[1];
+    const int n_lines = l == 0 ? a.n_in : a.n_out;
+    const int new_tiles = (total + TR - 1) / TR;
+    const int nblk = (n_lines + a.jb - 1) / a.jb;
+    const long long items = (long long)new_tiles * nblk;
+    // positions past the packed rows: no row, tile dead
+    for (long long i = (long long)new_tiles * TR + (long long)blockIdx.x * kThreads + tid;
+         i < (long long)a.n_tiles * TR; i += (long long)gridDim.x * kThreads)
+        rid_out[i] = -1;
+    for (int t = new_tiles + blockIdx.x * kThreads + tid; t < a.n_tiles; t += gridDim.x * kThreads)
+        a.alive_c[(size_t)t * AW + AW - 1] = 0u;
+    for (;;) {
+        if (tid == 0) sh.item = (long long)atomicAdd(&a.work[a.L + l], 1u);
+        __syncthreads();
+        const long long it = sh.item;
+        if (it >= items) break;
+        const int nt = (int)(it / nblk), bb = (int)(it % nblk);
+        // source of each new row: the g-th live row (ascending tiles, rows)
+        if (tid < TR) {
+            const int g = nt * TR + tid;
+            int s = -1;
+            if (g < total) {
+                int lo = 0, hi = a.n_tiles - 1;  // last tile with pre[t] <= g
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (pre[mid] <= g) lo = mid;
+                    else hi = mid - 1;
+                }
+                int rank = g - pre[lo];
+                const uint32_t* w = alive_l + (size_t)lo * AW;
+                for (int q = 0; q < AW - 1; ++q) {
+                    uint32_t word = __ldcg(&w[q]);
+                    const int c = __popc(word);
+                    if (rank < c) {
+                        for (; rank > 0; --rank) word &= word - 1u;
+                        s = lo * TR + q * 32 + (__ffs(word) - 1);
+                        break;
+                    }
+                    rank -= c;
+                }
+            }
+            sh.src[tid] = s;
+            if (bb == 0) {
+                rid_out[(size_t)nt * TR + tid] = s >= 0 ? rid_in[s] : -1;
+                const unsigned bw = __ballot_sync(0xffffffffu, s >= 0);
+                if (lane == 0) a.alive_c[(size_t)nt * AW + tid / 32] = bw;
+                if (tid == 0) a.alive_c[(size_t)nt * AW + AW - 1] = 1u;
+            }
+        }
+        __syncthreads();
+        int src[RPL];
+#pragma unroll
+        for (int c = 0; c < RPL; ++c) src[c] = sh.src[lane * RPL + c];
+        const int j0 = bb * a.jb, j1 = min(n_lines, j0 + a.jb);
+        const size_t tl_out = (size_t)nt * a.ld;
+        for (int k = j0 + warp; k < j1; k += kWarps) {
+            T v[RPL];
+            unsigned bits = 0u;
+#pragma unroll
+            for (int c = 0; c < RPL; ++c) {
+                v[c] = T(0);
+                const int s = src[c];
+                if (s >= 0) {
+                    const int ot = s / TR, orow = s % TR, sec = orow / RPL;
+                    const size_t tl = (size_t)ot * a.ld;
+                    const uint2 m = imeta[tl + k];
+                    if ((m.x >> sec) & 1u)
+                        v[c] = in[(tl * 32 + m.y + (unsigned)__popc(m.x & ((1u << sec) - 1u))) * RPL + orow % RPL];
+                }
+                bits |= (v[c] != T(0)) ? (1u << c) : 0u;
+            }
+            const unsigned om = __ballot_sync(0xffffffffu, bits != 0u);
+            const unsigned hb = (unsigned)k * 32u;
+            if (bits) st32(reinterpret_cast<char*>(out + (tl_out * 32 + hb + sector_pos(om, lane)) * RPL), v);
+            if (lane == 0) ometa[tl_out + k] = make_uint2(om, hb);
+        }
+        __syncthreads();  // sh.src / sh.item are rewritten by the next item
+    }
+}
+
 // All remaining layers (from a.first_l) in one cooperative launch with a
 // grid barrier between live layers.
 template <typename T, int GB, bool ZFILL>
@@ -1282,14 +1442,37 @@ __global__ void __launch_bounds__(kThreads, SDNN_NET_OCC)
     if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[a.first_l] = globaltimer();
 
     bool all_dead = false;
+    // compactions so far (an odd count flips the slab parity); kept in
+    // shared memory so the layer walk carries no extra register
+    __shared__ int s_gen;
+    if (tid == 0) s_gen = 0;
+    __syncthreads();
     for (int l = a.first_l; l < a.L; ++l) {
         // zero rows stay zero: once no tile is live every later layer is empty
         if (!all_dead && __ldcg(&a.tile_count[l]) == 0) all_dead = true;
         if (all_dead) continue;
-        layer_pass<T, GB, false, ZFILL>(a, l, tiles, sh);
+        const uint32_t* alive_in = nullptr;
+        int gen = s_gen;
+        if (a.compact_pct > 0) {
+            int total, live_tiles;
+            int* pre = tiles + a.n_tiles;  // [n_tiles + 1] live rows before each tile
+            row_prefix<T>(a.alive + (size_t)l * a.n_tiles * alive_words<T>(), a.n_tiles, pre, sh.scan_c, total,
+                          live_tiles);
+            const int new_tiles = (total + tile_rows<T>() - 1) / tile_rows<T>();
+            if (new_tiles < live_tiles &&
+                (long long)(live_tiles - new_tiles) * 100 >= (long long)a.compact_pct * live_tiles) {
+                compact_pass<T>(a, l, ((l ^ gen) & 1) != 0, gen, pre, total, sh);
+                grid_barrier(a.bar, nb);  // (its __syncthreads orders every read of s_gen before this write)
+                ++gen;
+                if (tid == 0) s_gen = gen;
+                alive_in = a.alive_c;
+            }
+        }
+        layer_pass<T, GB, false, ZFILL>(a, l, tiles, sh, ((l ^ gen) & 1) != 0, alive_in);
         grid_barrier(a.bar, nb);
         if (a.stamps && blockIdx.x == 0 && tid == 0) a.stamps[l + 1] = globaltimer();
     }
+    if (a.n_compact && blockIdx.x == 0 && tid == 0) *a.n_compact = s_gen;
 }
 
 // Read back the rows of each tile of the final slab, one warp per tile,

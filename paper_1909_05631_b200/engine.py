@@ -154,6 +154,7 @@ class RunResult:
     stage_ms: np.ndarray | None = None  # [densify, bit-line layer launch, persistent launch]
     h2d_bytes: int = 0          # end-to-end calls: host -> device bytes copied
     segments: int = 0           # end-to-end calls: row segments streamed
+    compactions: int = 0        # live-row repacks between layers
 
 
 class DeviceBatch:
@@ -279,6 +280,11 @@ class DeviceNetwork:
     def set_layer_timing(self, on: bool) -> None:
         _lib.check(_lib.lib().sdnn_net_set_layer_timing(self.handle, 1 if on else 0))
 
+    def set_compaction(self, pct: int) -> None:
+        """Repack live rows densely before a layer once that frees >= pct % of
+        the live tiles (<= 0: never).  Bit-identical results either way."""
+        _lib.check(_lib.lib().sdnn_net_set_compaction(self.handle, int(pct)))
+
     def weight_bytes(self) -> int:
         b = ctypes.c_int64()
         _lib.check(_lib.lib().sdnn_net_weight_bytes(self.handle, ctypes.byref(b)))
@@ -401,6 +407,8 @@ def _collect(h, n_rows: int, want_y: bool) -> RunResult:
         layer_ms = None
     stage_ms = np.zeros(3)
     _lib.check(L.sdnn_result_stage_ms(h, _lib.ptr(stage_ms)))
+    comp = ctypes.c_int64()
+    _lib.check(L.sdnn_result_compactions(h, ctypes.byref(comp)))
     y = None
     if want_y:
         nnz = ctypes.c_int64()
@@ -411,7 +419,7 @@ def _collect(h, n_rows: int, want_y: bool) -> RunResult:
         _lib.check(L.sdnn_result_y_csr(h, _lib.ptr(off), _lib.ptr(cols), _lib.ptr(vals)))
         y = (off, cols[:nnz.value], vals[:nnz.value])
     return RunResult(cats, live, L.sdnn_result_device_ms(h), L.sdnn_result_wall_ms(h),
-                     launches.value, y, layer_ms, stage_ms)
+                     launches.value, y, layer_ms, stage_ms, compactions=comp.value)
 
 
 # ------------------------------------------------------- network residency

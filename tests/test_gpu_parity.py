@@ -225,6 +225,47 @@ def test_large_n_live_rows_f32_and_f64(n):
         net.close()
 
 
+@pytest.mark.parametrize("dtype,prec", [("f64", 64), ("f32", 32)])
+@pytest.mark.parametrize("bits", ["1", "0"])
+def test_live_row_compaction_is_bit_identical(env, dtype, prec, bits):
+    """Rows die gradually here (2000 -> 1074 over 10 layers, every tile
+    keeps some): repacking the live rows densely between layers (SURVEY.md
+    7 step 3) only moves values, so every threshold -- never, whenever a
+    tile is freed, the default, rarely -- gives the oracle's bits, through
+    the device-side Y, the host assembly and multi-wave runs; bit-line
+    (binary) and float first layers."""
+    env["SDNN_BIN"] = bits
+    w, y0, layers = permunion_case(1024, 10, 2000, 0.125)
+    want = O.infer(layers, [w.bias] * w.layers, y0, precision=prec, threads=8)
+    cats = O.categorize(want)
+    assert 0 < cats.size < 1500
+    net = E.DeviceNetwork(w.n, 0, dtype)
+    net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias)
+    batch = net.upload_csr(y0.n_rows, y0.off, y0.cols, y0.vals)
+    runs = {}
+    for pct in (0, 1, 10, 60):
+        net.set_compaction(pct)
+        r = net.run(batch, w.ymax, want_y=True)
+        assert O.CSR(y0.n_rows, w.n, *r.y).identical(want), pct
+        assert np.array_equal(r.categories, cats), pct
+        runs[pct] = r
+    assert runs[0].compactions == 0
+    assert runs[1].compactions >= 2 and runs[10].compactions >= 1
+    for r in runs.values():
+        assert np.array_equal(r.live_rows, runs[0].live_rows)
+    net.set_compaction(1)
+    env["SDNN_HOST_Y"] = "1"
+    host = net.run(batch, w.ymax, want_y=True)
+    assert host.compactions >= 2
+    assert all(np.array_equal(a, b) for a, b in zip(host.y, runs[0].y))
+    env["SDNN_HOST_Y"] = "0"
+    env["SDNN_WAVE_ROWS"] = "700"
+    waves = net.run(batch, w.ymax, want_y=True)
+    assert waves.compactions >= 1
+    assert all(np.array_equal(a, b) for a, b in zip(waves.y, runs[0].y))
+    net.close()
+
+
 def test_wave_splitting_does_not_change_bits(env):
     env["SDNN_WAVE_ROWS"] = "37"
     w, y0, layers = permunion_case(1024, 4, 200, 0.125)
