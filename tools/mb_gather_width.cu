@@ -45,6 +45,9 @@ __device__ __forceinline__ void ld16(float (&d)[4], const char* p, bool live) {
 
 // MODE 0: 256-bit pieces.  MODE 1: 128-bit pieces, two loads per line.
 // MODE 2: 128-bit pieces, lane owns pieces 2l and 2l+1 (interleaved halves).
+// MODE 3: 32-byte sectors packed as in MODE 0 (a sector is stored when either
+//         half holds a nonzero), each half loaded by its own predicated
+//         128-bit load (half-sector live masks).
 template <int MODE>
 __global__ void gather(const char* __restrict__ buf, int iters, uint32_t thresh, float* out) {
     const int lane = threadIdx.x & 31;
@@ -69,7 +72,12 @@ __global__ void gather(const char* __restrict__ buf, int iters, uint32_t thresh,
             float d[4], e[4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) d[c] = e[c] = acc[c];
-            if (MODE == 1) {  // pieces l and 32 + l
+            if (MODE == 3) {  // sector-packed, two predicated halves
+                const unsigned ms = m0 | m1;
+                const char* sec = line + __popc(ms & below) * 32;
+                ld16(d, sec, l0);
+                ld16(e, sec + 16, l1);
+            } else if (MODE == 1) {  // pieces l and 32 + l
                 ld16(d, line + __popc(m0 & below) * 16, l0);
                 ld16(e, line + (__popc(m0) + __popc(m1 & below)) * 16, l1);
             } else {  // pieces 2l and 2l + 1 in one packed order
@@ -107,13 +115,15 @@ int main() {
         double p;
     } ps[] = {{"w32 p=0.34", 0, 0.34}, {"w16 halves p=0.185", 1, 0.185}, {"w16 interleaved p=0.185", 2, 0.185},
               {"w32 p=1.0", 0, 1.0},   {"w16 halves p=1.0", 1, 1.0},     {"w32 p=0.1", 0, 0.1},
-              {"w16 halves p=0.05", 1, 0.05}};
+              {"w16 halves p=0.05", 1, 0.05},  {"w16 sector-packed p=0.185", 3, 0.185},
+              {"w16 sector-packed p=1.0", 3, 1.0}};
     for (auto& q : ps) {
         const uint32_t th = q.p >= 1.0 ? 0xffffffffu : (uint32_t)(q.p * 4294967296.0);
         for (int rep = 0; rep < 2; ++rep) {
             cudaEventRecord(a);
             if (q.mode == 0) gather<0><<<grid, block>>>(buf, iters, th, out);
             else if (q.mode == 1) gather<1><<<grid, block>>>(buf, iters, th, out);
+            else if (q.mode == 3) gather<3><<<grid, block>>>(buf, iters, th, out);
             else gather<2><<<grid, block>>>(buf, iters, th, out);
             cudaEventRecord(b);
             CK(cudaEventSynchronize(b));
