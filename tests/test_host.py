@@ -85,3 +85,26 @@ def test_bench_shards_and_byte_model():
     assert b[2] == 0 and b[3] == 0
     assert b[1] == 4 * w.n * 90 * 2 + 8 * 32 * w.n
     assert b[0] == 1000 * 8 + 101 * 8 + 4 * w.n * 100 + 8 * 32 * w.n
+
+
+def test_bench_reference_arm_line_on_cpu():
+    """`bench.py --impl reference` (the driver's reference arm) runs on host
+    cores only and prints the contract's JSON line: impl, cpu_baseline with
+    its kind / cores / sample, an e2e object with zero copy bytes."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    out = subprocess.run([sys.executable, str(root / "bench.py"), "--impl", "reference", "--workload", "C1",
+                          "--batch", "3000", "--steps", "1", "--warmup", "1"],
+                         capture_output=True, text=True, timeout=600, cwd=str(root))
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0 and line["unit"] == "edges/s"
+    assert line["higher_is_better"] is True and line["steps"] == 1 and line["warmup"] == 1
+    cb = line["cpu_baseline"]
+    assert cb["kind"] in ("port", "reference") and cb["cores"] >= 1 and cb["sample"]
+    assert cb["value"] == line["value"]
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
