@@ -117,6 +117,10 @@ __host__ __device__ constexpr int tile_rows() { return 32 * rows_per_lane<T>(); 
 template <typename T>
 __host__ __device__ constexpr int alive_words() { return tile_rows<T>() / 32 + 1; }
 
+// Cache hint of the float line gathers (tuning knob; "" = default policy).
+#ifndef SDNN_GATHER_HINT
+#define SDNN_GATHER_HINT ""
+#endif
 // One lane's 32-byte sector <-> its RPL values (256-bit accesses).
 // Predicated 256-bit gather: zeros without any memory request when the
 // lane's sector is not live.
@@ -124,7 +128,7 @@ __device__ __forceinline__ void ld32_pred(float (&d)[8], const char* p, bool liv
     asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %9, 0;\n\t"
         "mov.b32 %0, 0;\n\tmov.b32 %1, 0;\n\tmov.b32 %2, 0;\n\tmov.b32 %3, 0;\n\t"
         "mov.b32 %4, 0;\n\tmov.b32 %5, 0;\n\tmov.b32 %6, 0;\n\tmov.b32 %7, 0;\n\t"
-        "@q ld.global.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n\t}"
+        "@q ld.global" SDNN_GATHER_HINT ".v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n\t}"
         : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3]), "=f"(d[4]), "=f"(d[5]), "=f"(d[6]), "=f"(d[7])
         : "l"(p), "r"((unsigned)live));
 }
@@ -140,7 +144,7 @@ __device__ __forceinline__ void ld32_pred(double (&d)[4], const char* p, bool li
 // lane's sector is not live (the caller zeroes the lane's weight instead).
 __device__ __forceinline__ void ld32_keep(float (&d)[8], const char* p, bool live) {
     asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %9, 0;\n\t"
-        "@q ld.global.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n\t}"
+        "@q ld.global" SDNN_GATHER_HINT ".v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n\t}"
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3]), "+f"(d[4]), "+f"(d[5]), "+f"(d[6]), "+f"(d[7])
         : "l"(p), "r"((unsigned)live));
 }
