@@ -266,6 +266,48 @@ def test_live_row_compaction_is_bit_identical(env, dtype, prec, bits):
     net.close()
 
 
+def _random_instance(rng):
+    """A general instance in the spirit of the reference's helpers.random_model /
+    random_batch (tests/helpers.py:31-50): mixed-sign weights avoiding 0,
+    variable degree, biases that may be positive, binary or real inputs."""
+    n = int(rng.integers(8, 97))
+    layers, bias = [], []
+    for _ in range(int(rng.integers(1, 9))):
+        dens = rng.uniform(0.02, 0.3)
+        w = np.where(rng.random((n, n)) < dens, rng.uniform(-1, 1, (n, n)), 0.0)
+        layers.append(O.CSR.from_dense(w))
+        bias.append(float(rng.uniform(-0.5, 0.2)))
+    rows = int(rng.integers(0, 300))
+    y = (rng.random((rows, n)) < rng.uniform(0.05, 0.6)).astype(np.float64)
+    if rng.random() < 0.5:
+        y *= rng.uniform(0.1, 2.0, y.shape)  # real-valued inputs: float densify path
+    return n, layers, bias, O.CSR.from_dense(y)
+
+
+@pytest.mark.parametrize("compact", ["0", "1"])
+def test_random_general_instances_f64_bit_exact(env, compact):
+    """200 random general instances (acceptance criterion 4's shape,
+    test_acceptance.py:231-250) through the C ABI in float64 against the
+    oracle bit for bit (the oracle is pinned to the reference by the
+    goldens), and in float32 against its float instance; with live-row
+    compaction off, and forced whenever it frees a tile."""
+    env["SDNN_COMPACT"] = compact
+    rng = np.random.default_rng(20261020)
+    for i in range(200):
+        n, layers, bias, y0 = _random_instance(rng)
+        for dtype, prec in (("f64", 64), ("f32", 32)):
+            if prec == 32 and i % 4:
+                continue
+            net = E.DeviceNetwork(n, 0, dtype)
+            for w, b in zip(layers, bias):
+                net.add_layer_csr(sm(w), b)
+            res = net.run(net.upload_csr(y0.n_rows, y0.off, y0.cols, y0.vals), 32.0, want_y=True)
+            want = O.infer(layers, bias, y0, precision=prec)
+            assert O.CSR(y0.n_rows, n, *res.y).identical(want), (i, dtype)
+            assert np.array_equal(res.categories, O.categorize(want)), (i, dtype)
+            net.close()
+
+
 def test_wave_splitting_does_not_change_bits(env):
     env["SDNN_WAVE_ROWS"] = "37"
     w, y0, layers = permunion_case(1024, 4, 200, 0.125)
