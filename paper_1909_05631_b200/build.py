@@ -37,16 +37,21 @@ def build(force: bool = False, verbose: bool = False) -> None:
         _run(["gcc", "-O3", "-std=gnu11", "-fPIC", "-shared", "-Wall", "-o", str(GENLIB),
               str(gen_src), "-lpthread"])
     cu = [CSRC / "sdnn.cu"]
-    deps = cu + [CSRC / "sdnn_kernels.cuh", gen_src, *headers]
+    host_src = CSRC / "sdnn_host.c"
+    deps = cu + [CSRC / "sdnn_kernels.cuh", gen_src, host_src, *headers]
     if force or _stale(LIB, deps):
         obj = PKG / "sdnn_gen.o"
+        hobj = PKG / "sdnn_host.o"
         _run(["gcc", "-O3", "-std=gnu11", "-fPIC", "-c", "-o", str(obj), str(gen_src)])
+        _run(["gcc", "-O3", "-std=gnu11", "-fPIC", "-mavx2", "-fopenmp", "-Wall", "-c", "-o", str(hobj),
+              str(host_src)])
         cmd = [NVCC, ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-fopenmp,-mavx2",
-               "-cudart", "static", "-o", str(LIB), *map(str, cu), str(obj), "-lpthread", "-lgomp"]
+               "-cudart", "static", "-o", str(LIB), *map(str, cu), str(obj), str(hobj), "-lpthread", "-lgomp"]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         _run(cmd)
         obj.unlink(missing_ok=True)
+        hobj.unlink(missing_ok=True)
 
 
 if __name__ == "__main__":

@@ -28,6 +28,11 @@
 
 #include <omp.h>
 
+// csrc/sdnn_host.c: AVX2 narrowing of int64 columns to uint16 with
+// non-temporal staging stores
+extern "C" void sdnn_host_narrow16(const int64_t* cc, const double* vv, uint16_t* d16, int64_t m, int64_t ncols,
+                                   int* bad, int* bin);
+
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
@@ -882,7 +887,9 @@ int upload_csr(sdnn_net* net, int64_t n_rows, const int64_t* off, const int64_t*
         const double* vv = vals + c0;
         const int64_t m = c1 - c0;
         const uint64_t ncu = (uint64_t)n_cols;
-        if (cb == 2) {
+        if (cb == 2 && (reinterpret_cast<uintptr_t>(dst) & 31) == 0 && env_int("SDNN_NARROW_AVX2", 1)) {
+            sdnn_host_narrow16(cc, vv, reinterpret_cast<uint16_t*>(dst), m, n_cols, &chunk_bad, &chunk_bin);
+        } else if (cb == 2) {
             uint16_t* d16 = reinterpret_cast<uint16_t*>(dst);
 #pragma omp parallel for simd reduction(| : chunk_bad) reduction(& : chunk_bin) schedule(static)
             for (int64_t p = 0; p < m; ++p) {

@@ -88,3 +88,42 @@ def test_nominal_edges_match_challenge_rate_arithmetic():
     w = W.CONFIGS["C1"]
     assert w.edges == 60000 * 1024 * 32 * 120
     assert W.CONFIGS["C4"].edges == 60000 * 65536 * 32 * 1920
+
+
+@pytest.mark.parametrize("m", [0, 5, 16, 17, 1000, 4099])
+def test_host_narrowing_of_y0_columns(m):
+    """The upload's host pass (csrc/sdnn_host.c: AVX2, non-temporal staging
+    stores): int64 columns -> uint16, range check, binary-value check; equal
+    to the plain conversion for every length (16-entry blocks + tail)."""
+    import ctypes
+
+    lib = _lib.lib()
+    f = lib.sdnn_host_narrow16
+    f.restype = None
+    f.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int64, ctypes.c_int64] + [ctypes.POINTER(ctypes.c_int)] * 2
+    rng = np.random.default_rng(m)
+    n = 65536
+    cols = rng.integers(0, n, m).astype(np.int64)
+    vals = np.ones(m)
+    raw = np.zeros(m + 32, np.uint16)
+    off = (-raw.ctypes.data % 32) // 2  # 32-byte aligned destination
+    dst = raw[off:off + m]
+
+    def run(c, v):
+        bad, binary = ctypes.c_int(0), ctypes.c_int(1)
+        f(c.ctypes.data, v.ctypes.data, dst.ctypes.data, m, n, ctypes.byref(bad), ctypes.byref(binary))
+        return bad.value, binary.value
+
+    assert run(cols, vals) == (0, 1)
+    assert np.array_equal(dst, cols.astype(np.uint16))
+    if m:
+        for at in (0, m - 1, m // 2):
+            v2 = vals.copy()
+            v2[at] = 0.5
+            assert run(cols, v2) == (0, 0)
+            v2[at] = np.nan
+            assert run(cols, v2) == (0, 0)
+            for badc in (-1, n, 1 << 40):
+                c2 = cols.copy()
+                c2[at] = badc
+                assert run(c2, vals)[0] == 1
