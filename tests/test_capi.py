@@ -127,3 +127,17 @@ def test_host_narrowing_of_y0_columns(m):
                 c2 = cols.copy()
                 c2[at] = badc
                 assert run(c2, vals)[0] == 1
+
+
+def test_null_handles_are_parameter_errors_without_a_gpu():
+    """Entry points that take a handle reject NULL with the parameter code
+    (2 -> ParameterError) before touching a device."""
+    import ctypes
+
+    lib = _lib.lib()
+    n = ctypes.c_int64()
+    assert lib.sdnn_net_set_compaction(None, 10) == 2
+    assert lib.sdnn_net_set_layer_timing(None, 1) == 2
+    assert lib.sdnn_result_compactions(None, ctypes.byref(n)) == 2
+    assert lib.sdnn_result_launches(None, ctypes.byref(n)) == 2
+    assert lib.sdnn_result_n_categories(None, ctypes.byref(n)) == 2
