@@ -178,7 +178,8 @@ int sdnn_result_launches(const sdnn_result *r, int64_t *n);
 /* Live-row compaction: before a layer, the live rows
  * are repacked densely into tiles when that frees at least `pct` % of the
  * live tiles (default 10; <= 0 never; the SDNN_COMPACT environment variable
- * overrides).  Results are bit-identical either way.  No reference
+ * overrides) and at least 16 tiles (SDNN_COMPACT_MIN).  Results are
+ * bit-identical either way.  No reference
  * counterpart: the reference's CSR rows carry no dead-row cost. */
 int sdnn_net_set_compaction(sdnn_net *net, int pct);
 /* Row compactions the run performed (summed over waves / segments). */

@@ -666,6 +666,10 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     a.n_compact = net->n_compact;
     // live-row compaction: repack once that % of the live tiles would be freed
     a.compact_pct = env_int("SDNN_COMPACT", net->compact_pct);
+    // ... and only when it frees at least this many tiles: a repack costs a
+    // pass over the live rows and a grid barrier (C1 as specified: 4 rows
+    // left in 4 tiles, repacking them cost more than it saved)
+    a.compact_min = std::max(1, env_int("SDNN_COMPACT_MIN", 16));
     a.jb = env_int("SDNN_JB", net->jb);
     const int kc = std::min(1024, env_int("SDNN_DENSIFY_KC", 96));  // input neurons per staging chunk
     const size_t dsmem = (size_t)kc * kLineBytes;

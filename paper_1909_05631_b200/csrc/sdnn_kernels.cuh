@@ -250,6 +250,7 @@ struct NetArgs {
                           // rowid[g & 1] and writes rowid[(g + 1) & 1]
     uint32_t* alive_c;    // [n_tiles][alive_words] row bitmap of the repacked tiles
     int compact_pct;      // repack when >= this % of the live tiles would be freed (<= 0: never)
+    int compact_min;      // ... and at least this many tiles (a repack costs a pass and a grid barrier)
     int* n_compact;       // compactions done (written by block 0 at the end)
 };
 
@@ -1463,7 +1464,7 @@ __global__ void __launch_bounds__(kThreads, SDNN_NET_OCC)
             row_prefix<T>(a.alive + (size_t)l * a.n_tiles * alive_words<T>(), a.n_tiles, pre, sh.scan_c, total,
                           live_tiles);
             const int new_tiles = (total + tile_rows<T>() - 1) / tile_rows<T>();
-            if (new_tiles < live_tiles &&
+            if (new_tiles < live_tiles && live_tiles - new_tiles >= a.compact_min &&
                 (long long)(live_tiles - new_tiles) * 100 >= (long long)a.compact_pct * live_tiles) {
                 compact_pass<T>(a, l, ((l ^ gen) & 1) != 0, gen, pre, total, sh);
                 grid_barrier(a.bar, nb);  // (its __syncthreads orders every read of s_gen before this write)

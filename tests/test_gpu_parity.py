@@ -235,6 +235,7 @@ def test_live_row_compaction_is_bit_identical(env, dtype, prec, bits):
     the device-side Y, the host assembly and multi-wave runs; bit-line
     (binary) and float first layers."""
     env["SDNN_BIN"] = bits
+    env["SDNN_COMPACT_MIN"] = "1"  # this batch spans 8-16 tiles
     w, y0, layers = permunion_case(1024, 10, 2000, 0.125)
     want = O.infer(layers, [w.bias] * w.layers, y0, precision=prec, threads=8)
     cats = O.categorize(want)
@@ -292,6 +293,7 @@ def test_random_general_instances_f64_bit_exact(env, compact):
     goldens), and in float32 against its float instance; with live-row
     compaction off, and forced whenever it frees a tile."""
     env["SDNN_COMPACT"] = compact
+    env["SDNN_COMPACT_MIN"] = "1"
     rng = np.random.default_rng(20261020)
     for i in range(200):
         n, layers, bias, y0 = _random_instance(rng)
