@@ -2,28 +2,33 @@
 """Benchmark of the Sparse DNN inference loop on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload C4] [--dtype f32|f64]
+                    [--workload C4] [--dtype f32|f64] [--scaling strong|weak]
 
 A step is one pass of the whole network (all L layers plus the category
 list) over the batch, the reference's timed region (engine.py:336-339).
 Default workload: C4, the flagship (N=65536, L=1920, 60,000 rows), which
-fits one B200.  With N GPUs (torchrun, one process per GPU) every rank holds
-a full weight replica; rows are independent, so by default (--scaling weak)
-every rank runs a full batch of its own distinct rows and `value` counts the
-rows of all ranks; --scaling strong splits one batch into contiguous row
-blocks (the reference's data-parallel tiling).  There is no per-layer
-collective, only the final category gather and a max-over-ranks of the
-device time.
+fits one B200.
 
-`value`: nominal edges/s (inputs x N x 32 x L / t, challenge.py:131-135) with
-Y0 already resident in HBM, device time from CUDA events on the engine's
-stream.  `e2e`: the same metric through the C ABI with host buffers (H2D of
-Y0 and D2H of the categories inside the timed region).  `e2e_images`: the
-same network fed raw 28x28 images resized on the device (the reference's
-ingest.resize_threshold_flatten).  `roofline`: the
-dominant layer launch against measured HBM bandwidth.  `cpu_baseline`: the
-oracle port (a C restatement of the reference engine, oracle/) on the host
-cores over a row sample.  `--impl reference` prints that CPU arm alone.
+Multi-GPU: one process per GPU.  `--gpus N` without a torchrun environment
+re-launches this script under `torch.distributed.run` with N ranks (NCCL on
+GPUs, gloo without).  Every rank holds a full weight replica; by default
+(`--scaling strong`, north_star) the one 60,000-row batch is split into
+contiguous row blocks (the reference's data-parallel tiling,
+engine.py:222,237-251) and `value` is the batch's edges over the slowest
+rank's device time.  With N > 1 a `weak` field adds the other reading:
+every rank a full batch of its own rows.  There is no per-layer
+collective, only the final category gather and max-over-ranks reductions.
+
+`value`: nominal edges/s (inputs x N x 32 x L / t, challenge.py:131-135)
+with Y0 resident in HBM, device time from CUDA events on the engine's
+stream.  `e2e`: the same metric through the C ABI with host buffers (the
+reference's int64/float64 CSR in, H2D of Y0 and D2H of the categories
+inside the timed region).  `roofline`: the dominant launch against
+measured HBM bandwidth.  `cpu_baseline` / `--impl reference`: the
+UNMODIFIED reference engine (`sdnnbench.engine.infer_timed`, numba,
+data-parallel over every host core, float64) from `baseline/_ref` on a
+bounded sample of the same workload, extrapolated to the full batch (the
+oracle's C port stands in only when the reference is not installed).
 """
 
 from __future__ import annotations
@@ -31,12 +36,12 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
 import tempfile
 import time
-from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
 import numpy as np
@@ -45,11 +50,13 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 from paper_1909_05631_b200 import workloads as W  # noqa: E402
+from paper_1909_05631_b200.dist import RankGroup, shard  # noqa: E402
 
 METRIC = "edges/sec (inputs×N×32×L / time)"
 UNIT = "edges/s"
 PEAKS = ROOT / "MEASURED_PEAKS.json"
 HBM_FALLBACK = 6650.0  # B200_PROFILING.md fallback, GB/s
+REF_DIR = ROOT / "baseline" / "_ref"
 
 
 def hbm_peak():
@@ -57,6 +64,16 @@ def hbm_peak():
         return float(json.loads(PEAKS.read_text())["hbm_gbs"]), "measured"
     except Exception:  # noqa: BLE001
         return HBM_FALLBACK, "fallback"
+
+
+def cpu_model() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:  # noqa: BLE001
+        pass
+    return "unknown"
 
 
 # -------------------------------------------------------------- clocks
@@ -68,12 +85,14 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, device: int):
+    def __init__(self, device):
         self.device = device
         self.proc = None
         self.file = None
 
     def start(self):
+        if self.device is None:
+            return self
         try:
             self.file = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
             self.proc = subprocess.Popen(
@@ -82,6 +101,7 @@ class ClockSampler:
                 stdout=self.file, stderr=subprocess.DEVNULL)
         except Exception:  # noqa: BLE001
             self.proc = None
+        return self
 
     def stop(self, window=None):
         """Summarise the samples; with window=(t0, t1) (time.time() of the
@@ -126,11 +146,6 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(rows), "scope": scope}
 
 
-# ---------------------------------------------------------- distributed
-
-from paper_1909_05631_b200.dist import RankGroup, shard  # noqa: E402
-
-
 # ----------------------------------------------------------- byte model
 
 def layer_bytes(w: W.Workload, elem: int, live: np.ndarray, nnz0: int, rows: int) -> np.ndarray:
@@ -164,158 +179,317 @@ def measured_traffic(w: W.Workload, rows: int, dtype: str, kernel: str):
     return None
 
 
-# ------------------------------------------------------------ CPU oracle
+# ------------------------------------------------- CPU baseline (reference)
 
-def cpu_sample(w: W.Workload, rows: int, precision: int, threads: int):
-    """Time the oracle port (C restatement of the reference engine) on a
-    `rows`-row sample through all L layers; weights are generated per layer
-    batch outside the clock (the reference loads its model before timing)."""
-    from oracle import oracle as O
-    from paper_1909_05631_b200 import _lib
+def reference_engine():
+    """(sdnnbench.engine, sdnnbench.model) of the UNMODIFIED reference from
+    baseline/_ref (offline pip install of /root/reference; travels to the
+    GPU box with the repo), or None when it is not installed."""
+    if not (REF_DIR / "sdnnbench" / "engine.py").exists():
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(tempfile.gettempdir(), "sdnn_numba_cache"))
+    if str(REF_DIR) not in sys.path:
+        sys.path.append(str(REF_DIR))
+    try:
+        from sdnnbench import engine, model
+    except Exception:  # noqa: BLE001 -- e.g. numba missing: the port stands in
+        return None
+    return engine, model
 
-    off, cols, vals = W.images(w, n_rows=rows)
-    y = O.CSR(rows, w.n, off, cols, vals)
-    g = _lib.gen()
-    t_compute = 0.0
-    batch = max(1, threads)
-    idx = np.zeros((batch, w.n, w.width), np.int32)
-    ones = np.full(w.n * w.width, w.value, np.float64)
 
-    def to_csr(i):
-        o = np.zeros(w.n + 1, np.int64)
-        c = np.zeros(w.n * w.width, np.int64)
-        v = np.zeros(w.n * w.width, np.float64)
-        _lib.check_gen(g.sdnn_gen_ell_to_csr(w.n, w.n, w.width, _lib.ptr(idx[i]), _lib.ptr(ones),
-                                             _lib.ptr(o), _lib.ptr(c), _lib.ptr(v)))
-        return O.CSR(w.n, w.n, o, c, v)
-
-    with ThreadPoolExecutor(max_workers=batch) as pool:
-        for l0 in range(0, w.layers, batch):
-            m = min(batch, w.layers - l0)
-            _lib.check_gen(g.sdnn_gen_permunion_ell_layers(w.weight_seed, l0, m, w.n, w.width,
-                                                           threads, _lib.ptr(idx)))
-            csrs = list(pool.map(to_csr, range(m)))
-            for lw in csrs:
-                t0 = time.perf_counter()
-                y = O.infer([lw], [w.bias], y, w.ymax, precision=precision, threads=threads)
-                t_compute += time.perf_counter() - t0
-    return t_compute, O.categorize(y)
+LEAD_LAYERS = 8    # layers timed on the row sample (as specified, rows die by layer 2-3)
+DEAD_LAYERS = 16   # layers timed on the full batch of empty rows
 
 
 def cpu_rows_for(w: W.Workload) -> int:
     if w.value > 0.1:  # live companions: rows saturate and stay dense
-        return 8
-    return {1024: 20000, 4096: 4000, 16384: 1500, 65536: 400}.get(w.n, 400)
+        return 64
+    return {1024: 60000, 4096: 20000, 16384: 6000, 65536: 2000}.get(w.n, 2000)
+
+
+class CpuBaseline:
+    """The reference's inference loop on the host cores over a bounded
+    sample of workload `w`, extrapolated to the full batch.
+
+    A step times (a) the first `lead` layers over `S` rows of Y0 (rows are
+    independent, engine.py:237-251), scaled by B/S, and (b) when every
+    sampled row is dead after them, the remaining layers as `dead`
+    distinct layers over the full B-row batch of empty rows (zero rows stay
+    zero; their cost is the per-row loop of engine.py:81-83), scaled by
+    (L - lead) / dead.  If sampled rows are still alive after the lead
+    layers, (a) is scaled by L / lead instead.  `kind` "reference" runs
+    sdnnbench.engine.infer_timed itself (mode data_parallel, one worker per
+    host core, float64); "port" the oracle's C restatement (float64), used
+    only when the reference is not installed."""
+
+    def __init__(self, w: W.Workload, rows: int, threads: int, prefer: str = "reference"):
+        self.w, self.threads = w, threads
+        self.S = max(1, min(w.batch, rows))
+        self.lead = min(w.layers, LEAD_LAYERS)
+        self.dead = min(w.layers - self.lead, DEAD_LAYERS)
+        layers = W.layers_csr(w, 0, self.lead + self.dead, threads)
+        off, cols, vals = W.images(w, n_rows=self.S, threads=threads)
+        ref = reference_engine() if prefer == "reference" else None
+        self.kind = "reference" if ref else "port"
+        if ref:
+            self.RE, M = ref
+            lw = [M.LayerWeights(M.SparseMatrix(w.n, w.n, *c, check=False), w.bias) for c in layers]
+            self.lead_model = M.NetworkModel(w.n, tuple(lw[:self.lead]))
+            self.dead_model = M.NetworkModel(w.n, tuple(lw[self.lead:])) if self.dead else None
+            self.y0 = M.FeatureBatch(M.SparseMatrix(self.S, w.n, off, cols, vals, check=False))
+            self.empty = M.FeatureBatch(M.SparseMatrix.empty(w.batch, w.n))
+            self.cfg = self.RE.InferenceConfig(ymax=w.ymax, mode="data_parallel", workers=threads)
+        else:
+            from oracle import oracle as O
+
+            self.O = O
+            cs = [O.CSR(w.n, w.n, *c) for c in layers]
+            self.lead_model, self.dead_model = cs[:self.lead], cs[self.lead:]
+            self.y0 = O.CSR(self.S, w.n, off, cols, vals)
+            self.empty = O.CSR(w.batch, w.n, np.zeros(w.batch + 1, np.int64), np.zeros(0, np.int64),
+                               np.zeros(0))
+        self.live_after = None
+
+    def _timed(self, model, y):
+        """(seconds, rows alive after) of one timed region: infer + categorize."""
+        if self.kind == "reference":
+            _, cats, sec = self.RE.infer_timed(model, y, self.cfg)
+            return sec, len(cats)
+        t0 = time.perf_counter()
+        out = self.O.infer(model, [self.w.bias] * len(model), y, self.w.ymax, precision=64,
+                           threads=self.threads)
+        cats = self.O.categorize(out)
+        return time.perf_counter() - t0, int(cats.size)
+
+    def step(self) -> float:
+        """Extrapolated seconds of one full-batch pass."""
+        w = self.w
+        t_lead, alive = self._timed(self.lead_model, self.y0)
+        self.live_after = alive
+        t = t_lead * w.batch / self.S
+        if self.lead < w.layers:
+            if alive == 0 and self.dead:
+                t_dead, _ = self._timed(self.dead_model, self.empty)
+                t += t_dead * (w.layers - self.lead) / self.dead
+            else:
+                t *= w.layers / self.lead
+        return t
+
+    def describe(self) -> str:
+        w = self.w
+        eng = ("sdnnbench.engine.infer_timed (the unmodified reference from baseline/_ref, numba), "
+               f"mode=data_parallel, workers={self.threads}, float64"
+               if self.kind == "reference" else
+               f"oracle/ C port of engine.py:64-137,192-251 (reference not installed), {self.threads} "
+               "threads, float64")
+        s = f"{eng}; {self.S} of {w.batch} rows through layers 1-{self.lead}"
+        if self.S < w.batch:
+            s += f" x {w.batch / self.S:.1f} (rows)"
+        if self.lead < w.layers:
+            if self.live_after == 0 and self.dead:
+                s += (f"; every sampled row dead after layer {self.lead}, so layers {self.lead + 1}-{w.layers}"
+                      f" timed as {self.dead} layers over the full {w.batch}-row batch of empty rows"
+                      f" x {(w.layers - self.lead) / self.dead:.1f} (layers)")
+            else:
+                s += f"; {self.live_after} sampled rows still alive, x {w.layers / self.lead:.1f} (layers)"
+        extrap = self.S < w.batch or self.lead < w.layers
+        return s + ("; extrapolated" if extrap else "; full workload") + f"; CPU: {cpu_model()}"
+
+
+def cpu_baseline(w: W.Workload, rows: int = 0, prefer: str = "reference") -> dict:
+    """One bounded CPU-baseline measurement for our line (rank 0, N=1):
+    one untimed warm-up step (numba specialises on the read-only arrays)
+    and one timed step."""
+    threads = os.cpu_count() or 1
+    cb = CpuBaseline(w, rows or cpu_rows_for(w), threads, prefer)
+    cb.step()
+    t = cb.step()
+    return {"value": w.edges / t, "unit": UNIT, "cores": threads, "kind": cb.kind,
+            "sample": cb.describe(), "seconds_extrapolated": t, "dtype": "f64"}
 
 
 # ------------------------------------------------------------ our arm
 
-def run_ours(args, dist: RankGroup):
-    import torch
+class DeviceArm:
+    """This rank's row block on its GPU through the product path
+    (libsdnn.so via the package's DeviceNetwork).  Weights: with N > 1,
+    rank 0 generates the device ELL and the others receive it by NCCL
+    broadcast over NVLink/NVSwitch (untimed setup)."""
 
-    from paper_1909_05631_b200.engine import DeviceNetwork
+    def __init__(self, args, dist: RankGroup, w: W.Workload, r0: int, r1: int):
+        import torch
 
+        from paper_1909_05631_b200.engine import DeviceNetwork
+
+        self.torch, self.args, self.dist, self.w = torch, args, dist, w
+        self.device = dist.local
+        self.rows = r1 - r0
+        threads = host_threads()
+        self.net = net = DeviceNetwork(w.n, self.device, args.dtype)
+        weights = args.weights if args.weights != "auto" else ("broadcast" if dist.world > 1 else "generate")
+        if weights == "broadcast" and dist.world > 1:
+            if dist.rank == 0:
+                net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias,
+                                         threads=os.cpu_count() or 1)
+            else:
+                net.add_layers_uninit(w.layers, w.width, w.bias)
+            dist.broadcast_layers(net, 0, w.layers)
+        else:
+            net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias, threads=threads)
+        self.off, self.cols, self.vals = W.images(w, n_rows=self.rows, row0=r0, threads=threads)
+        self.nnz0 = int(self.off[-1])
+        self.batch = net.upload_csr(self.rows, self.off, self.cols, self.vals)
+
+    def sync(self):
+        self.torch.cuda.synchronize(self.device)
+
+    def step(self):
+        return self.net.run(self.batch, self.w.ymax)
+
+    def extras(self, ms_per_step: float, steps: int) -> dict:
+        """Roofline (per-launch CUDA events), e2e through the C ABI."""
+        args, dist, w, net = self.args, self.dist, self.w, self.net
+        elem = 8 if args.dtype == "f64" else 4
+        net.set_layer_timing(True)
+        prof = net.run(self.batch, w.ymax)
+        net.set_layer_timing(False)
+        lb = layer_bytes(w, elem, prof.live_rows, self.nnz0, self.rows)
+        live_layers = np.nonzero(prof.live_rows[:-1] > 0)[0]
+        peak, peak_kind = hbm_peak()
+        live_ms = float(prof.layer_ms[live_layers].sum()) if live_layers.size else 0.0
+        all_gbs = lb.sum() / (live_ms * 1e-3) / 1e9 if live_ms > 0 else 0.0
+        # dominant launch of the timed steps: the bit-line first-layer launch
+        # covers layer 1, the persistent launch the rest
+        stage_ms = dist.max_array(self.stage_ms / steps)
+        bin_first = stage_ms[1] > 0
+        launch_bytes = [0.0, float(lb[0]) if bin_first else 0.0, float(lb[1:].sum() if bin_first else lb.sum())]
+        names = ["densify_kernel (Y0 -> tiles)", "bin_layer_kernel (layer 1, bit-line tiles)",
+                 f"net_kernel (layers {2 if bin_first else 1}-{w.layers}, persistent)"]
+        dom = int(np.argmax(stage_ms))
+        dom_gbs = launch_bytes[dom] / (stage_ms[dom] * 1e-3) / 1e9 if stage_ms[dom] > 0 else 0.0
+        traffic = measured_traffic(w, self.rows, args.dtype, names[dom].split()[0])
+        live_total = dist.sum(float(prof.live_rows[:-1].sum()))
+
+        # end to end through the C ABI with host buffers (sdnn_infer_streamed,
+        # the call engine.infer makes): host CSR conversion + H2D of Y0 in row
+        # segments overlapped with the run of earlier segments, + D2H of the
+        # category list
+        e2e_ms = 0.0
+        for i in range(steps + 1):
+            t0 = time.perf_counter()
+            r2 = net.infer_csr(self.rows, self.off, self.cols, self.vals, w.ymax, want_y=False)
+            _ = r2.categories.copy()
+            dt = (time.perf_counter() - t0) * 1e3
+            if i > 0:  # first call grows the pinned staging buffer
+                e2e_ms += dt
+        e2e_ms = dist.max(e2e_ms / steps)
+        t0 = time.perf_counter()
+        b2 = net.upload_csr(self.rows, self.off, self.cols, self.vals)
+        t1 = time.perf_counter()
+        r3 = net.run(b2, w.ymax)
+        _ = r3.categories.copy()
+        t2 = time.perf_counter()
+        b2.close()
+        total_edges = self.total_edges
+        return {
+            "live": {
+                "rows_entering_each_live_layer": [int(x) for x in prof.live_rows[:-1][live_layers][:8]],
+                "live_layers": int(live_layers.size),
+                "live_edges_per_s": live_total * w.n * w.width / (ms_per_step * 1e-3),
+            },
+            "roofline": {
+                "bound": "hbm",
+                "achieved": dom_gbs,
+                "peak": peak,
+                "unit": "GB/s",
+                "frac": dom_gbs / peak,
+                "traffic": traffic["bytes"] if traffic else None,
+                "traffic_source": traffic["source"] if traffic else None,
+                "kernel": names[dom],
+                "per_launch_ms": float(stage_ms[dom]),
+                "algorithmic_bytes": launch_bytes[dom],
+                "launch_ms": {"densify": round(float(stage_ms[0]), 3), "bin_layer": round(float(stage_ms[1]), 3),
+                              "net": round(float(stage_ms[2]), 3)},
+                "all_live_layers_gbs": all_gbs,
+                "live_layer_ms": [round(float(prof.layer_ms[l]), 3) for l in live_layers[:8]],
+                "peak_kind": peak_kind,
+            },
+            "e2e": {
+                "value": total_edges / (e2e_ms * 1e-3),
+                "unit": UNIT,
+                "h2d_bytes_per_step": int(r2.h2d_bytes),
+                "d2h_bytes_per_step": (w.layers + 1) * 4 + int(r2.live_rows[-1]) * 4,
+                "ms_per_step": e2e_ms,
+                "segments": int(r2.segments),
+                "unstreamed_upload_then_run_ms": [round((t1 - t0) * 1e3, 1), round((t2 - t1) * 1e3, 1)],
+            },
+        }
+
+    def weak(self, steps: int) -> dict:
+        """Weak-scaling reading (N > 1): every rank a full batch of its own
+        distinct rows (rank g: rows g*B ... (g+1)*B - 1 of the seeded image
+        stream), same network."""
+        dist, w = self.dist, self.w
+        off, cols, vals = W.images(w, n_rows=w.batch, row0=dist.rank * w.batch, threads=host_threads())
+        b = self.net.upload_csr(w.batch, off, cols, vals)
+        del off, cols, vals
+        for _ in range(2):
+            self.net.run(b, w.ymax)
+        dist.barrier()
+        self.sync()
+        ms = sum(self.net.run(b, w.ymax).device_ms for _ in range(steps)) / steps
+        self.sync()
+        dist.barrier()
+        b.close()
+        ms = dist.max(ms)
+        return {"value": w.edges * dist.world / (ms * 1e-3), "ms_per_step": ms,
+                "global_batch": w.batch * dist.world, "steps": steps,
+                "note": "every GPU a full batch of its own distinct rows"}
+
+    def close(self):
+        self.batch.close()
+        self.net.close()
+
+
+def run_ours(args, dist: RankGroup, arm_cls=None):
+    """Generic rank logic: shard, warm up, time exactly K steps between
+    barriers + device syncs, max over ranks, gather categories.  `arm_cls`
+    is the per-rank executor (DeviceArm; the CPU tests inject a stand-in
+    to exercise this logic under gloo)."""
     w = workload(args)
-    dev = dist.local
     if args.scaling == "weak":  # every rank a full batch of its own rows (rows are independent)
         r0, r1 = dist.rank * w.batch, (dist.rank + 1) * w.batch
     else:  # the batch row-partitioned over the ranks (engine._infer_data_parallel tiling)
         r0, r1 = shard(w.batch, dist.rank, dist.world)
-    rows = r1 - r0
     total_edges = w.edges * (dist.world if args.scaling == "weak" else 1)
     global_batch = w.batch * (dist.world if args.scaling == "weak" else 1)
-    elem = 8 if args.dtype == "f64" else 4
-    threads = host_threads()
     t_setup = time.perf_counter()
-    net = DeviceNetwork(w.n, dev, args.dtype)
-    weights = args.weights if args.weights != "auto" else ("broadcast" if dist.world > 1 else "generate")
-    if weights == "broadcast" and dist.world > 1:
-        # rank 0 generates (with every host core), the others receive the
-        # device ELL over NCCL (NVLink/NVSwitch): untimed setup, SURVEY.md 8e
-        if dist.rank == 0:
-            net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias,
-                                     threads=os.cpu_count() or 1)
-        else:
-            net.add_layers_uninit(w.layers, w.width, w.bias)
-        dist.broadcast_layers(net, 0, w.layers)
-    else:
-        net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias, threads=threads)
-    off, cols, vals = W.images(w, n_rows=rows, row0=r0, threads=threads)
-    nnz0 = int(off[-1])
-    batch = net.upload_csr(rows, off, cols, vals)
+    arm = (arm_cls or DeviceArm)(args, dist, w, r0, r1)
+    arm.total_edges = total_edges
     setup_s = time.perf_counter() - t_setup
 
-    clocks = ClockSampler(dev)
-    clocks.start()  # before the warm-up, so nvidia-smi is sampling by the timed region
+    clocks = ClockSampler(getattr(arm, "device", None)).start()  # sampling by the timed region
     for _ in range(args.warmup):
-        net.run(batch, w.ymax)
+        arm.step()
     dist.barrier()
-    torch.cuda.synchronize(dev)
+    arm.sync()
     t_region0 = time.time()
-    dev_ms, wall0 = 0.0, time.perf_counter()
-    launches = 0
+    dev_ms, wall0, launches = 0.0, time.perf_counter(), 0
     stage_ms = np.zeros(3)
     for _ in range(args.steps):
-        res = net.run(batch, w.ymax)
+        res = arm.step()
         dev_ms += res.device_ms
         launches += res.launches
         stage_ms += res.stage_ms
-    torch.cuda.synchronize(dev)
+    arm.sync()
     wall_ms = (time.perf_counter() - wall0) * 1e3
     t_region1 = time.time()
     dist.barrier()
     clk = clocks.stop((t_region0, t_region1))
+    arm.stage_ms = stage_ms
     ms_per_step = dist.max(dev_ms / args.steps)
     wall_per_step = dist.max(wall_ms / args.steps)
     cats = dist.gather_categories(res.categories, r0)
-    live_total = dist.sum(float(res.live_rows[:-1].sum()))
-
-    # profiling pass (untimed): per-layer events for the roofline
-    net.set_layer_timing(True)
-    prof = net.run(batch, w.ymax)
-    net.set_layer_timing(False)
-    lb = layer_bytes(w, elem, prof.live_rows, nnz0, rows)
-    live_layers = np.nonzero(prof.live_rows[:-1] > 0)[0]
-    peak, peak_kind = hbm_peak()
-    live_ms = float(prof.layer_ms[live_layers].sum()) if live_layers.size else 0.0
-    all_gbs = lb.sum() / (live_ms * 1e-3) / 1e9 if live_ms > 0 else 0.0
-    # dominant launch of the timed steps (CUDA events on the engine's stream):
-    # the bit-line first-layer launch covers layer 1, the persistent launch
-    # the rest; its algorithmic bytes are those of the layers it ran
-    stage_ms = dist.max_array(stage_ms / args.steps)
-    bin_first = stage_ms[1] > 0
-    launch_bytes = [0.0, float(lb[0]) if bin_first else 0.0, float(lb[1:].sum() if bin_first else lb.sum())]
-    names = ["densify_kernel (Y0 -> tiles)", "bin_layer_kernel (layer 1, bit-line tiles)",
-             f"net_kernel (layers {2 if bin_first else 1}-{w.layers}, persistent)"]
-    dom = int(np.argmax(stage_ms))
-    dom_gbs = launch_bytes[dom] / (stage_ms[dom] * 1e-3) / 1e9 if stage_ms[dom] > 0 else 0.0
-    traffic = measured_traffic(w, rows, args.dtype, names[dom].split()[0])
-
-    # end to end through the C ABI with host buffers (sdnn_infer_streamed,
-    # the call engine.infer makes): host CSR conversion + H2D of Y0 in row
-    # segments overlapped with the run of earlier segments, + D2H of the
-    # category list
-    e2e_ms = 0.0
-    for i in range(args.steps + 1):
-        t0 = time.perf_counter()
-        r2 = net.infer_csr(rows, off, cols, vals, w.ymax, want_y=False)
-        _ = r2.categories.copy()
-        dt = (time.perf_counter() - t0) * 1e3
-        if i > 0:  # first call grows the pinned staging buffer
-            e2e_ms += dt
-    e2e_ms = dist.max(e2e_ms / args.steps)
-    h2d = r2.h2d_bytes
-    d2h = (w.layers + 1) * 4 + int(r2.live_rows[-1]) * 4
-    # the same call unstreamed, for the split: upload, then run
-    t0 = time.perf_counter()
-    b2 = net.upload_csr(rows, off, cols, vals)
-    t1 = time.perf_counter()
-    r3 = net.run(b2, w.ymax)
-    _ = r3.categories.copy()
-    t2 = time.perf_counter()
-    b2.close()
-    e2e_split = [round((t1 - t0) * 1e3, 1), round((t2 - t1) * 1e3, 1)]
-    images = images_e2e(args, w, net) if dist.world == 1 else None
 
     line = {
         "metric": METRIC,
@@ -339,63 +513,56 @@ def run_ours(args, dist: RankGroup):
                             + ", weight replica per GPU, no per-layer collective"),
             "l2": "inputs larger than L2 (Y0 CSR and weights exceed 126 MB; no flush)",
         },
-        "live": {
-            "rows_entering_each_live_layer": [int(x) for x in prof.live_rows[:-1][live_layers][:8]],
-            "live_layers": int(live_layers.size),
-            "live_edges_per_s": live_total * w.n * w.width / (ms_per_step * 1e-3),
-            "categories": int(cats.size),
-        },
-        "roofline": {
-            "bound": "hbm",
-            "achieved": dom_gbs,
-            "peak": peak,
-            "unit": "GB/s",
-            "frac": dom_gbs / peak,
-            "traffic": traffic["bytes"] if traffic else None,
-            "traffic_source": traffic["source"] if traffic else None,
-            "kernel": names[dom],
-            "per_launch_ms": float(stage_ms[dom]),
-            "algorithmic_bytes": launch_bytes[dom],
-            "launch_ms": {"densify": round(float(stage_ms[0]), 3), "bin_layer": round(float(stage_ms[1]), 3),
-                          "net": round(float(stage_ms[2]), 3)},
-            "all_live_layers_gbs": all_gbs,
-            "live_layer_ms": [round(float(prof.layer_ms[l]), 3) for l in live_layers[:8]],
-            "peak_kind": peak_kind,
-        },
-        "e2e": {
-            "value": total_edges / (e2e_ms * 1e-3),
-            "unit": UNIT,
-            "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h,
-            "ms_per_step": e2e_ms,
-            "segments": int(r2.segments),
-            "unstreamed_upload_then_run_ms": e2e_split,
-        },
+        "categories": int(cats.size),
         "gpu_launches": launches,
         "wall_ms_per_step": wall_per_step,
-        **({"e2e_images": images} if images else {}),
         "clocks": clk,
-        "setup_s": setup_s,
+        "setup_s": dist.max(setup_s),
     }
-    batch.close()
-    net.close()
-    if args.companions and dist.world == 1:
-        line["companions"] = companions(args, net_cls=DeviceNetwork)
+    if hasattr(arm, "extras"):
+        line.update(arm.extras(ms_per_step, args.steps))
+    if dist.world > 1 and args.scaling == "strong" and hasattr(arm, "weak") and not args.no_weak:
+        line["weak"] = arm.weak(min(args.steps, 5))
+    if dist.world == 1 and hasattr(arm, "net"):
+        if not args.no_images:
+            images = images_e2e(args, w, arm.net)
+            if images:
+                line["e2e_images"] = images
+    arm.close()
+    if dist.world == 1 and arm_cls is None:
+        if args.also_f64 and args.dtype == "f32":
+            line["f64"] = f64_line(args, w)
+        if args.companions:
+            line["companions"] = companions(args)
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
-        S = args.cpu_rows or cpu_rows_for(w)
-        t_cpu, _ = cpu_sample(w, S, 64 if args.dtype == "f64" else 32, threads)
-        line["cpu_baseline"] = {
-            "value": S * w.n * w.width * w.layers / t_cpu,
-            "unit": UNIT,
-            "cores": threads,
-            "kind": "port",
-            "sample": f"{S} of {w.batch} rows through all {w.layers} layers, oracle/ C port of "
-                      f"engine._spmm_kernel+_bias_relu_clamp_kernel, {threads} threads, "
-                      f"{'float64' if args.dtype == 'f64' else 'float32'}",
-            "seconds": t_cpu,
-        }
+        line["cpu_baseline"] = cpu_baseline(w, args.cpu_rows)
     return line
+
+
+def f64_line(args, w: W.Workload) -> dict:
+    """The same workload on the bit-exact float64 path (the reference's
+    arithmetic), N=1: a second field beside the float32 headline."""
+    from paper_1909_05631_b200.engine import DeviceNetwork
+
+    net = DeviceNetwork(w.n, 0, "f64")
+    net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias)
+    off, cols, vals = W.images(w)
+    b = net.upload_csr(w.batch, off, cols, vals)
+    for _ in range(3):
+        net.run(b, w.ymax)
+    steps = max(3, min(args.steps, 10))
+    clocks = ClockSampler(0).start()
+    t0 = time.time()
+    runs = [net.run(b, w.ymax) for _ in range(steps)]
+    clk = clocks.stop((t0, time.time()))
+    ms = sum(r.device_ms for r in runs) / steps
+    stage = sum(r.stage_ms for r in runs) / steps
+    b.close()
+    net.close()
+    return {"value": w.edges / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "steps": steps,
+            "launch_ms": {"densify": round(float(stage[0]), 3), "bin_layer": round(float(stage[1]), 3),
+                          "net": round(float(stage[2]), 3)},
+            "categories": int(runs[-1].categories.size), "clocks": clk}
 
 
 def images_e2e(args, w: W.Workload, net):
@@ -405,7 +572,7 @@ def images_e2e(args, w: W.Workload, net):
     ingest.resize_threshold_flatten) and run through the workload's network,
     categories back; beside it the same rows through the host-CSR call."""
     side = int(round(w.n ** 0.5))
-    if args.no_images or side * side != w.n or side not in (32, 64, 128, 256):
+    if side * side != w.n or side not in (32, 64, 128, 256):
         return None
     pix = W.stroke_images(w.batch)
     b = net.upload_images(pix, side)  # warm-up; its CSR feeds the host-CSR comparison
@@ -438,21 +605,31 @@ def images_e2e(args, w: W.Workload, net):
     }
 
 
-def companions(args, net_cls):
-    """Live-row companion (K2 at C5 depth): rows stay alive and saturate,
-    so every layer carries the full batch.  One warm-up, one timed step."""
+def companions(args):
+    """Live-row companions (default K2 at C5 depth: rows stay alive and
+    saturate, so every layer carries the full batch): 2 warm-up steps, at
+    least 3 timed steps with their own clock record."""
+    from paper_1909_05631_b200.engine import DeviceNetwork
+
     out = []
     for spec in args.companions.split(","):
         name, _, L = spec.partition(":")
         w = W.CONFIGS[name]
         if L:
             w = w.with_(layers=int(L))
-        net = net_cls(w.n, 0, args.dtype)
+        net = DeviceNetwork(w.n, 0, args.dtype)
         net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias)
         off, cols, vals = W.images(w)
         b = net.upload_csr(w.batch, off, cols, vals)
-        net.run(b, w.ymax)
-        r = net.run(b, w.ymax)
+        for _ in range(2):
+            net.run(b, w.ymax)
+        steps = 3
+        clocks = ClockSampler(0).start()
+        t0 = time.time()
+        runs = [net.run(b, w.ymax) for _ in range(steps)]
+        clk = clocks.stop((t0, time.time()))
+        ms = sum(r.device_ms for r in runs) / steps
+        r = runs[-1]
         net.set_compaction(0)  # the same run without live-row compaction, for comparison
         r0 = net.run(b, w.ymax)
         net.set_compaction(10)
@@ -462,17 +639,20 @@ def companions(args, net_cls):
         lb = layer_bytes(w, elem, p.live_rows, int(off[-1]), w.batch)
         peak, _ = hbm_peak()
         mid = w.layers // 2
+        gbs = lb[mid] / (p.layer_ms[mid] * 1e-3) / 1e9 if p.layer_ms[mid] > 0 else 0.0
         out.append({
             "workload": f"{w.name}: N={w.n}, L={w.layers}, batch={w.batch}, w={w.value}",
-            "value": w.edges / (r.device_ms * 1e-3),
-            "ms_per_step": r.device_ms,
+            "value": w.edges / (ms * 1e-3),
+            "ms_per_step": ms,
+            "steps": steps,
+            "clocks": clk,
             "live_rows_last_layer": int(p.live_rows[-2]),
             "categories": int(r.categories.size),
             "row_compactions": int(r.compactions),
             "ms_per_step_without_compaction": r0.device_ms,
             "steady_layer_ms": float(p.layer_ms[mid]),
-            "steady_layer_gbs": lb[mid] / (p.layer_ms[mid] * 1e-3) / 1e9 if p.layer_ms[mid] > 0 else 0,
-            "steady_layer_frac": (lb[mid] / (p.layer_ms[mid] * 1e-3) / 1e9) / peak if p.layer_ms[mid] > 0 else 0,
+            "steady_layer_gbs": gbs,
+            "steady_layer_frac": gbs / peak,
         })
         b.close()
         net.close()
@@ -482,19 +662,19 @@ def companions(args, net_cls):
 # ------------------------------------------------------ reference arm
 
 def run_reference(args, dist: RankGroup):
+    """The driver's reference arm: the reference's own CPU implementation of
+    the path on the host cores (CpuBaseline), same workload/metric/unit.
+    Under torchrun only rank 0 works and prints."""
     if dist.rank != 0:
         return None
     w = workload(args)
     threads = os.cpu_count() or 1
-    S = args.cpu_rows or cpu_rows_for(w)
-    prec = 64 if args.dtype == "f64" else 32
-    for _ in range(args.warmup):
-        cpu_sample(w, S, prec, threads)
-    secs = [cpu_sample(w, S, prec, threads)[0] for _ in range(args.steps)]
+    cb = CpuBaseline(w, args.cpu_rows or cpu_rows_for(w), threads)
+    for _ in range(max(1, args.warmup)):  # >= 1: numba specialises on the first real call
+        cb.step()
+    secs = [cb.step() for _ in range(args.steps)]
     t = sum(secs) / len(secs)
-    value = S * w.n * w.width * w.layers / t
-    sample = (f"{S} of {w.batch} rows through all {w.layers} layers per step, oracle/ C port of "
-              f"the reference engine (engine.py:64-137,192-251), {threads} threads")
+    value = w.edges / t
     return {
         "metric": METRIC,
         "value": value,
@@ -504,20 +684,22 @@ def run_reference(args, dist: RankGroup):
         "warmup": args.warmup,
         "ms_per_step": t * 1e3,
         "higher_is_better": True,
-        "scaling": "strong",
+        "scaling": args.scaling,
         "vs_baseline": None,
-        "dtype": args.dtype,
+        "dtype": "f64",
         "data": "synthetic (seeded perm-union weights, Bernoulli images; BASELINE.json config)",
         "config": {"workload": f"{w.name}: N={w.n}, L={w.layers}, batch={w.batch}, p={w.p}, "
-                               f"w={w.value}, bias={w.bias}",
+                               f"w={w.value}, bias={w.bias}, ymax={w.ymax}",
                    "neurons": w.n, "layers": w.layers, "global_batch": w.batch,
-                   "parallelism": "host threads"},
+                   "parallelism": f"host threads ({threads}); the reference has no GPU path"},
         "impl": "reference",
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": cb.kind,
+                         "sample": cb.describe()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
+
+# --------------------------------------------------------------- launch
 
 def host_threads() -> int:
     """Host threads per rank: the node's cores split over its local ranks."""
@@ -534,10 +716,30 @@ def workload(args) -> W.Workload:
         kw["batch"] = args.batch
     if args.p is not None:
         kw["p"] = args.p
+    if args.weight_value is not None:
+        kw["value"] = args.weight_value
     return w.with_(**kw) if kw else w
 
 
-def main(argv=None):
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(n: int, argv) -> int:
+    """Re-launch this script under torch.distributed.run with n ranks on
+    this node (the driver's own launch line), return its exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()),
+           *argv]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # the init log shows every rank joining
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return subprocess.call(cmd, env=env)
+
+
+def parser():
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -545,19 +747,38 @@ def main(argv=None):
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--weights", choices=("auto", "generate", "broadcast"), default="auto",
                     help="N>1: rank 0 generates, NCCL broadcast to the others (auto), or every rank generates")
-    ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
-                    help="weak: every GPU a full batch of its own rows; strong: one batch split over GPUs")
+    ap.add_argument("--scaling", choices=("strong", "weak"), default="strong",
+                    help="strong: one batch split over the GPUs (north_star); weak: every GPU a full batch")
+    ap.add_argument("--no-weak", action="store_true", help="N>1: skip the extra weak-scaling field")
     ap.add_argument("--workload", default="C4", choices=sorted(W.CONFIGS))
     ap.add_argument("--dtype", choices=("f32", "f64"), default="f32")
     ap.add_argument("--layers", type=int, default=0)
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--p", type=float, default=None)
+    ap.add_argument("--weight-value", type=float, default=None,
+                    help="override the workload's weight value (0.125: the live K2 regime)")
     ap.add_argument("--cpu-rows", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-images", action="store_true", help="skip the end-to-end-from-images line")
+    ap.add_argument("--also-f64", dest="also_f64", action="store_true", default=None,
+                    help="N=1, f32: add the workload on the float64 path (default for C4)")
+    ap.add_argument("--no-f64", dest="also_f64", action="store_false")
     ap.add_argument("--companions", default="K2:120",
                     help="comma list NAME[:LAYERS] of live companions ('' to skip)")
-    args = ap.parse_args(argv)
+    return ap
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else list(argv)
+    args = parser().parse_args(argv)
+    if args.also_f64 is None:
+        args.also_f64 = args.workload == "C4" and not (args.layers or args.batch or args.p is not None
+                                                       or args.weight_value is not None)
+    world = int(os.environ.get("WORLD_SIZE", "0") or 0)
+    if world == 0 and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus, argv))
+    if world and world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     os.environ.setdefault("OMP_NUM_THREADS", str(host_threads()))  # libsdnn's upload threads
     dist = RankGroup()
     try:

@@ -19,7 +19,9 @@ def _bases(name, own):
     return (own, ref) if ref is not None and ref is not own else (own,)
 
 
-class SdnnError(*(((Exception, _ref.SdnnError) if _ref is not None else (Exception,)))):
+# the reference's SdnnError already derives from Exception: listing both
+# (Exception, _ref.SdnnError) has no consistent MRO
+class SdnnError(*((_ref.SdnnError,) if _ref is not None else (Exception,))):
     """Base class for all package errors."""
 
 

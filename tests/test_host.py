@@ -34,14 +34,6 @@ def test_error_codes_map_to_reference_classes():
     assert isinstance(errors.from_code(4, "x"), errors.ShapeError)
 
 
-def test_reference_error_classes_are_honoured_when_present():
-    ref = errors._ref
-    if ref is None:
-        pytest.skip("reference package not importable here")
-    assert issubclass(errors.ShapeError, ref.ShapeError)
-    assert issubclass(errors.ParameterError, ref.ParameterError)
-
-
 def test_stage_partition():  # engine.py:226-229
     assert E._stage_partition(10, 3) == [(0, 3), (3, 6), (6, 10)]
     assert E._stage_partition(5, 5) == [(i, i + 1) for i in range(5)]
