@@ -168,7 +168,7 @@ int sdnn_net_set_layer_timing(sdnn_net *net, int on);
 /* Per-layer device milliseconds of a run made with layer timing on. */
 int sdnn_result_layer_ms(const sdnn_result *r, double *ms);
 /* Device milliseconds of the run's launches, from CUDA events recorded on
- * the engine's stream in every run: ms[0] = Y0 expansion into tiles
+ * the engine's stream in every run: ms[0] = live-row select + Y0 expansion into tiles
  * (densify), ms[1] = the first layer's own launch over bit-line tiles (0
  * when Y0 is not binary), ms[2] = the persistent launch over the remaining
  * layers. */
@@ -189,6 +189,35 @@ int sdnn_result_compactions(const sdnn_result *r, int64_t *n);
 int sdnn_result_y_nnz(sdnn_result *r, int64_t *nnz);
 int sdnn_result_y_csr(sdnn_result *r, int64_t *off, int64_t *cols, double *vals);
 void sdnn_result_free(sdnn_result *r);
+
+/* ---- One handle over several GPUs -------------------
+ * engine._infer_data_parallel (engine.py:237-251) with one GPU per worker:
+ * every member holds a full weight replica; sdnn_group_infer splits the
+ * batch into contiguous row blocks of ceil(B / G) rows (engine.py:240), runs
+ * each block on its GPU from its own host thread (sdnn_infer_streamed:
+ * upload overlapped with the run), and merges the results in row order --
+ * bit-identical to one GPU.  Device time of a group result is the slowest
+ * member's (they run concurrently); launches, live rows, H2D bytes add up. */
+typedef struct sdnn_group sdnn_group;
+/* GPUs 0 .. n_gpus-1 (n_gpus <= 0: every visible GPU). */
+int sdnn_open(int n_gpus, int dtype, int64_t n_neurons, sdnn_group **out);
+/* An explicit device list (a device may appear more than once). */
+int sdnn_open_devices(const int *devices, int n_devices, int dtype, int64_t n_neurons,
+                      sdnn_group **out);
+void sdnn_close(sdnn_group *group);
+int sdnn_group_size(const sdnn_group *group, int *n);
+/* Member i's single-GPU handle (owned by the group; NULL if out of range). */
+sdnn_net *sdnn_group_net(sdnn_group *group, int i);
+/* Layers are converted once on the first member and replicated to the
+ * others device to device (peer copies over NVLink/NVSwitch). */
+int sdnn_group_add_layer_csr(sdnn_group *group, const int64_t *w_off, const int64_t *w_cols,
+                             const double *w_vals, int64_t nnz, double bias);
+int sdnn_group_add_layers_permunion(sdnn_group *group, uint64_t seed, int64_t first_layer,
+                                    int64_t count, int32_t width, double value, double bias,
+                                    int threads);
+int sdnn_group_infer(sdnn_group *group, int64_t n_rows, const int64_t *y_off,
+                     const int64_t *y_cols, const double *y_vals, double ymax, int want_y,
+                     sdnn_result **out);
 
 /* engine.spmm: Z = Y * W (n_rows x n_inner times n_inner x n_out), exact
  * zeros dropped, no epilogue.  Result Y is Z. */

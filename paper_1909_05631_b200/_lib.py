@@ -65,6 +65,14 @@ SIGNATURES = [
     ("sdnn_result_free", None, [vp]),
     ("sdnn_spmm", cint, [cint, cint, i64, i64, i64, vp, vp, vp, vp, vp, vp, P(vp)]),
     ("sdnn_bias_relu_clamp", cint, [cint, cint, i64, i64, vp, vp, vp, dbl, dbl, P(vp)]),
+    ("sdnn_open", cint, [cint, cint, i64, P(vp)]),
+    ("sdnn_open_devices", cint, [vp, cint, cint, i64, P(vp)]),
+    ("sdnn_close", None, [vp]),
+    ("sdnn_group_size", cint, [vp, P(cint)]),
+    ("sdnn_group_net", vp, [vp, cint]),
+    ("sdnn_group_add_layer_csr", cint, [vp, vp, vp, vp, i64, dbl]),
+    ("sdnn_group_add_layers_permunion", cint, [vp, u64, i64, i64, i32, dbl, dbl, cint]),
+    ("sdnn_group_infer", cint, [vp, i64, vp, vp, vp, dbl, cint, P(vp)]),
 ]
 
 GEN_SIGNATURES = [

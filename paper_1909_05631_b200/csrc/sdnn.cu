@@ -203,6 +203,13 @@ struct sdnn_result {
     }
 };
 
+// One handle over several GPUs: a network replica per device (devices may
+// repeat), the batch split into contiguous row blocks, one host thread per
+// device (engine._infer_data_parallel, engine.py:237-251, one GPU per worker).
+struct sdnn_group {
+    std::vector<sdnn_net*> nets;
+};
+
 namespace {
 
 int set_device(const sdnn_net* net) {
@@ -596,6 +603,9 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
         CK(cudaMalloc(&net->cub_tmp, tmp_bytes));
         net->cub_cap = tmp_bytes;
     }
+    // the run's device time starts here: the live-row select, the host round
+    // trip for its count and the scratch clears are part of the timed pass
+    CK(cudaEventRecord(net->ev0, net->stream));
     CK(cub::DeviceSelect::If(net->cub_tmp, tmp_bytes, it, net->rowlist, net->n_sel, (int)rows, pred, net->stream));
     int32_t n_live = 0;
     CK(cudaMemcpyAsync(&n_live, net->n_sel, 4, cudaMemcpyDeviceToHost, net->stream));
@@ -692,7 +702,6 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     occ = std::min(occ, std::max(1, env_int("SDNN_OCC", occ)));
     const int grid = net->sm_count * occ;
     void* args[] = {(void*)&a};
-    CK(cudaEventRecord(net->ev0, net->stream));
     bool quad = false;  // layer 1 over quad bit-lines (binary Y0, float)
     if (n_tiles) {
         // lines densify does not touch stay {mask 0}: zero the meta first
@@ -702,9 +711,11 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
         const bool bin = batch->vals == nullptr && env_int("SDNN_BIN", 1) != 0;
         a.bin_in = bin ? 1 : 0;
         if (bin) {  // binary Y0: bit-line tiles
-            quad = sizeof(T) == 4 && env_int("SDNN_QUAD", 1) != 0;
-            if (quad)  // quad lines of dead neurons / missing tiles must read as zero
-                CK(cudaMemsetAsync(a.slab[0], 0, (size_t)((n_tiles + 3) / 4) * ld * 128, net->stream));
+            quad = env_int("SDNN_QUAD", 1) != 0;
+            constexpr int TPQ = quad_tiles<T>();
+            if (quad)  // group lines of dead neurons / missing tiles must read as zero
+                CK(cudaMemsetAsync(a.slab[0], 0, (size_t)((n_tiles + TPQ - 1) / TPQ) * ld * kQuadLine,
+                                   net->stream));
             const int kcb = 1024;
             const int span = (int)(((n_in + spans - 1) / spans + kcb - 1) / kcb * kcb);
             const int64_t blocks = n_tiles * ((n_in + span - 1) / span);
@@ -727,12 +738,11 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
         res->launches += 1;
     }
     CK(cudaEventRecord(net->ev_d, net->stream));
-    if (a.bin_in && quad) {  // layer 1 over quad bit-lines (float): its own launch
-        const void* qfn = (const void*)bin_quad_kernel;
+    if (a.bin_in && quad) {  // layer 1 over quad / oct bit-lines: its own launch
+        const void* qfn = (const void*)bin_quad_kernel<T>;
         int qocc = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&qocc, qfn, kThreads, 0));
-        bin_quad_kernel<<<net->sm_count * std::max(qocc, 1), kThreads, 0, net->stream>>>(
-            *reinterpret_cast<NetArgs<float>*>(&a));
+        bin_quad_kernel<T><<<net->sm_count * std::max(qocc, 1), kThreads, 0, net->stream>>>(a);
         CK(cudaGetLastError());
         res->launches += 1;
         a.first_l = 1;
@@ -1401,6 +1411,37 @@ int infer_streamed(sdnn_net* net, int64_t n_rows, const int64_t* off, const int6
     return rc;
 }
 
+// Layers [first, end) of the group's first network copied to every other
+// member, device to device (a peer copy over NVLink/NVSwitch between GPUs;
+// untimed, like the reference's model loading).
+int replicate_layers(sdnn_group* g, size_t first) {
+    sdnn_net* src = g->nets[0];
+    for (size_t i = 1; i < g->nets.size(); ++i) {
+        sdnn_net* dst = g->nets[i];
+        if (int rc = set_device(dst)) return rc;
+        if (dst->device != src->device) {
+            int can = 0;
+            CK(cudaDeviceCanAccessPeer(&can, dst->device, src->device));
+            if (can) {
+                const cudaError_t e = cudaDeviceEnablePeerAccess(src->device, 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else CK(e);
+            }
+        }
+        for (size_t l = first; l < src->layers.size(); ++l) {
+            const DevLayer& S = src->layers[l];
+            DevLayer L = S;
+            const size_t slots = std::max<size_t>((size_t)S.wp * (size_t)src->n, 1);
+            CK(cudaMalloc(&L.idx, slots * sizeof(int32_t)));
+            CK(cudaMalloc(&L.val, slots * src->elem));
+            CK(cudaMemcpyPeer(L.idx, dst->device, S.idx, src->device, slots * sizeof(int32_t)));
+            CK(cudaMemcpyPeer(L.val, dst->device, S.val, src->device, slots * src->elem));
+            dst->layers.push_back(L);
+        }
+    }
+    return SDNN_OK;
+}
+
 }  // namespace
 
 // ===================================================================== C ABI
@@ -1885,6 +1926,144 @@ int sdnn_result_y_csr(sdnn_result* r, int64_t* off, int64_t* cols, double* vals)
 }
 
 void sdnn_result_free(sdnn_result* r) { delete r; }
+
+int sdnn_open_devices(const int* devices, int n_devices, int dtype, int64_t n_neurons, sdnn_group** out) {
+    if (!out || !devices || n_devices < 1) return fail(SDNN_ERR_PARAMETER, "bad device list");
+    sdnn_group* g = new sdnn_group;
+    for (int i = 0; i < n_devices; ++i) {
+        sdnn_net* net = nullptr;
+        if (int rc = make_net(devices[i], dtype, n_neurons, &net)) {
+            sdnn_close(g);
+            return rc;
+        }
+        g->nets.push_back(net);
+    }
+    *out = g;
+    return SDNN_OK;
+}
+
+int sdnn_open(int n_gpus, int dtype, int64_t n_neurons, sdnn_group** out) {
+    int count = 0;
+    CK(cudaGetDeviceCount(&count));
+    if (n_gpus <= 0) n_gpus = count;
+    if (n_gpus > count) return fail(SDNN_ERR_PARAMETER, "%d GPUs requested, %d visible", n_gpus, count);
+    std::vector<int> devs(std::max(n_gpus, 1));
+    for (int i = 0; i < n_gpus; ++i) devs[i] = i;
+    return sdnn_open_devices(devs.data(), n_gpus, dtype, n_neurons, out);
+}
+
+void sdnn_close(sdnn_group* g) {
+    if (!g) return;
+    for (auto* net : g->nets) sdnn_net_destroy(net);
+    delete g;
+}
+
+int sdnn_group_size(const sdnn_group* g, int* n) {
+    if (!g || !n) return fail(SDNN_ERR_PARAMETER, "null argument");
+    *n = (int)g->nets.size();
+    return SDNN_OK;
+}
+
+sdnn_net* sdnn_group_net(sdnn_group* g, int i) {
+    if (!g || i < 0 || i >= (int)g->nets.size()) return nullptr;
+    return g->nets[i];
+}
+
+int sdnn_group_add_layer_csr(sdnn_group* g, const int64_t* w_off, const int64_t* w_cols, const double* w_vals,
+                             int64_t nnz, double bias) {
+    if (!g) return fail(SDNN_ERR_PARAMETER, "null argument");
+    const size_t first = g->nets[0]->layers.size();
+    if (int rc = sdnn_net_add_layer_csr(g->nets[0], w_off, w_cols, w_vals, nnz, bias)) return rc;
+    return replicate_layers(g, first);
+}
+
+int sdnn_group_add_layers_permunion(sdnn_group* g, uint64_t seed, int64_t first_layer, int64_t count,
+                                    int32_t width, double value, double bias, int threads) {
+    if (!g) return fail(SDNN_ERR_PARAMETER, "null argument");
+    const size_t first = g->nets[0]->layers.size();
+    if (int rc = sdnn_net_add_layers_permunion(g->nets[0], seed, first_layer, count, width, value, bias, threads))
+        return rc;
+    return replicate_layers(g, first);
+}
+
+int sdnn_group_infer(sdnn_group* g, int64_t n_rows, const int64_t* y_off, const int64_t* y_cols,
+                     const double* y_vals, double ymax, int want_y, sdnn_result** out) {
+    if (!g || !out || n_rows < 0 || (n_rows > 0 && !y_off)) return fail(SDNN_ERR_PARAMETER, "bad batch");
+    if (n_rows > 0 && y_off[0] != 0) return fail(SDNN_ERR_PARAMETER, "row_offsets[0] must be 0");
+    const int G = (int)g->nets.size();
+    const int64_t L = (int64_t)g->nets[0]->layers.size();
+    for (auto* net : g->nets)
+        if ((int64_t)net->layers.size() != L) return fail(SDNN_ERR_PARAMETER, "group members hold different layers");
+    const double t0 = now_ms();
+    const int64_t per = std::max<int64_t>(1, (n_rows + G - 1) / G);  // engine.py:240 tile
+    struct Block {
+        int64_t r0 = 0, r1 = 0;
+        std::vector<int64_t> off;
+        sdnn_result* res = nullptr;
+        int rc = 0;
+        std::string err;
+    };
+    std::vector<Block> blk(G);
+    const int hw = host_threads();
+    std::vector<std::thread> workers;
+    for (int i = 0; i < G; ++i) {
+        Block& b = blk[i];
+        b.r0 = std::min<int64_t>(n_rows, i * per);
+        b.r1 = std::min<int64_t>(n_rows, b.r0 + per);
+        workers.emplace_back([&, i] {
+            Block& b = blk[i];
+            omp_set_num_threads(std::max(2, hw / G));  // the host cores shared by the blocks' producers
+            const int64_t rows = b.r1 - b.r0, c0 = rows > 0 ? y_off[b.r0] : 0;
+            b.off.resize(rows + 1);
+            for (int64_t r = 0; r <= rows; ++r) b.off[r] = (rows > 0 ? y_off[b.r0 + r] : 0) - c0;
+            b.rc = sdnn_infer_streamed(g->nets[i], rows, b.off.data(), y_cols ? y_cols + c0 : y_cols,
+                                       y_vals ? y_vals + c0 : y_vals, ymax, want_y, 0, &b.res);
+            if (b.rc == SDNN_OK && want_y) b.rc = y_to_host(b.res);
+            if (b.rc) b.err = g_err;
+        });
+    }
+    for (auto& t : workers) t.join();
+    int rc = SDNN_OK;
+    for (auto& b : blk)
+        if (b.rc && rc == SDNN_OK) {
+            rc = b.rc;
+            g_err = b.err;
+        }
+    sdnn_result* res = nullptr;
+    if (rc == SDNN_OK) {
+        res = new sdnn_result;
+        res->n_rows = n_rows;
+        res->n_cols = g->nets[0]->n;
+        res->n_layers = L;
+        res->live.assign(L + 1, 0);
+        if (want_y) {
+            res->off.assign(n_rows + 1, 0);
+            res->have_y = true;
+        }
+        for (auto& b : blk) {  // row order; the devices ran concurrently: device time is the slowest's
+            const sdnn_result& p = *b.res;
+            for (int64_t c : p.cats) res->cats.push_back(c + b.r0);
+            for (size_t l = 0; l < p.live.size() && l < res->live.size(); ++l) res->live[l] += p.live[l];
+            res->dev_ms = std::max(res->dev_ms, p.dev_ms);
+            for (int k = 0; k < 3; ++k) res->stage_ms[k] = std::max(res->stage_ms[k], p.stage_ms[k]);
+            res->launches += p.launches;
+            res->compactions += p.compactions;
+            res->h2d_bytes += p.h2d_bytes;
+            res->segments += p.segments;
+            if (want_y) {
+                const int64_t base = res->off[b.r0];
+                for (int64_t r = 1; r <= b.r1 - b.r0; ++r) res->off[b.r0 + r] = base + p.off[r];
+                res->cols.insert(res->cols.end(), p.cols.begin(), p.cols.end());
+                res->vals.insert(res->vals.end(), p.vals.begin(), p.vals.end());
+            }
+        }
+        res->wall_ms = now_ms() - t0;
+    }
+    for (auto& b : blk) delete b.res;
+    if (rc) return rc;
+    *out = res;
+    return SDNN_OK;
+}
 
 int sdnn_spmm(int device, int dtype, int64_t n_rows, int64_t n_inner, int64_t n_out, const int64_t* y_off,
               const int64_t* y_cols, const double* y_vals, const int64_t* w_off, const int64_t* w_cols,

@@ -555,11 +555,13 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_bin_kernel(const int6
                     stage[at] = 0u;
                     any |= wv[q];
                 }
-                if (any && quad) {  // quad layout: tile t's 32 bytes of quad line (t / 4, k)
+                if (any && quad) {  // quad layout: tile t's W*4 bytes of 128-byte line (t / TPQ, k)
+                    constexpr int TPQ = 32 / W;  // tiles per line: 4 (float), 8 (double)
                     uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<char*>(slab0) +
-                                                          ((size_t)(t >> 2) * ld + (k0 + k)) * 128 + (t & 3) * 32);
+                                                          ((size_t)(t / TPQ) * ld + (k0 + k)) * 128 +
+                                                          (t % TPQ) * (W * 4));
                     dst[0] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-                    dst[1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
+                    if (W == 8) dst[1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
                     gm[k0 + k] = make_uint2(0xFFFFFFFFu, (unsigned)(k0 + k));
                 } else if (any) {
                     const unsigned base = atomicAdd(&heap0[t], 1u);
@@ -1080,41 +1082,54 @@ __global__ void __launch_bounds__(kThreads, bin_occ<T>()) bin_layer_kernel(NetAr
         layer_pass<T, bin_gb<T>(), true, false>(a, 0, reinterpret_cast<int32_t*>(smem), sh);
 }
 
-// ------------------------------------- layer 1 over quad bit-lines (float)
-// Binary Y0 with four consecutive tiles interleaved: the 128-byte quad line
-// (quad q, neuron k) holds the 32-byte bit-lines of tiles 4q .. 4q+3 one
-// after the other (densify_bin_kernel, quad mode), so lane l reads ONE
-// 32-bit word per slot -- 32 rows (32*(l%8) .. +31) of tile 4q + l/8 -- and
-// a slot list, its loads and its loop serve 1,024 rows instead of 256.  The
-// per-column epilogue writes each lane's four float sectors into its tile's
-// line; a tile's kept-sector mask is assembled from its eight lanes'
-// nibbles by three shuffles.  Quad lines of dead tiles / neurons are zero
-// (the quad slab is cleared before densify), and a zero line adds nothing.
+// ------------------------------- layer 1 over quad (float) / oct (double) bit-lines
+// Binary Y0 with consecutive tiles interleaved: the 128-byte line (group q,
+// neuron k) holds the bit-lines of TPQ consecutive tiles one after the other
+// (densify_bin_kernel, quad mode): four 32-byte float bit-lines (256-row
+// tiles) or eight 16-byte double bit-lines (128-row tiles).  Lane l reads
+// ONE 32-bit word per slot -- 32 rows of tile TPQ*q + l/LPT -- so a slot
+// list, its loads and its loop serve 1,024 rows whatever the precision.
+// Per set bit the row's chain takes acc + w (= acc + y*w with y = 1, one
+// rounding, the same bits as the reference's mulsd + addsd and the float
+// path's fma).  The per-column epilogue writes each lane's 32 rows as its
+// tile's sectors (four of 8 floats / eight of 4 doubles); a tile's
+// kept-sector mask is assembled from its lanes' pieces by shuffles.  Lines
+// of dead tiles / neurons are zero (the slab is cleared before densify), and
+// a zero line adds nothing.
 #ifndef SDNN_QUAD_GB
 #define SDNN_QUAD_GB 2
 #endif
 #ifndef SDNN_QUAD_OCC
-#define SDNN_QUAD_OCC 3  // 80 registers, no spills (2: 6.0 ms, 4: spills, 5.3 ms)
+#define SDNN_QUAD_OCC 3  // float: 80 registers, no spills (2: 6.0 ms, 4: spills, 5.3 ms)
 #endif
-constexpr int kQuadLine = 128;  // bytes per (quad, neuron) line
+#ifndef SDNN_OCT_OCC
+#define SDNN_OCT_OCC 2  // double: 32 double accumulators
+#endif
+constexpr int kQuadLine = 128;  // bytes per (group, neuron) line
+template <typename T>
+__host__ __device__ constexpr int quad_tiles() { return sizeof(T) == 4 ? 4 : 8; }
+template <typename T>
+__host__ __device__ constexpr int quad_occ() { return sizeof(T) == 4 ? SDNN_QUAD_OCC : SDNN_OCT_OCC; }
 
-template <int GB>
-__device__ __forceinline__ void bin_quad_item(const NetArgs<float>& a, const LayerDesc<float>& L, int q,
-                                              int j0, int j1, uint2* wlist) {
-    constexpr int AW = alive_words<float>();
+template <typename T, int GB>
+__device__ __forceinline__ void bin_quad_item(const NetArgs<T>& a, const LayerDesc<T>& L, int q, int j0, int j1,
+                                              uint2* wlist) {
+    constexpr int AW = alive_words<T>(), RPL = rows_per_lane<T>();
+    constexpr int TPQ = quad_tiles<T>(), LPT = 32 / TPQ;  // lanes per tile: 8 (float), 4 (double)
+    constexpr int SPL = 32 / RPL;                        // sectors per lane: 4 (float), 8 (double)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int T = lane >> 3, sub = lane & 7;  // this lane's tile within the quad, its row group
+    const int T_ = lane / LPT, sub = lane % LPT;  // this lane's tile within the group, its 32-row word
     const unsigned below = (1u << lane) - 1u;
-    const int t0 = q * 4, ntq = min(4, a.n_tiles - t0);
-    const int t = t0 + min(T, ntq - 1);
-    const bool tile_ok = T < ntq;
+    const int t0 = q * TPQ, ntq = min(TPQ, a.n_tiles - t0);
+    const int t = t0 + min(T_, ntq - 1);
+    const bool tile_ok = T_ < ntq;
     const unsigned* inq = reinterpret_cast<const unsigned*>(reinterpret_cast<const char*>(a.slab[0]) +
                                                             (size_t)q * a.ld * kQuadLine) + lane;
     asm("mov.b64 %0, %0;" : "+l"(inq));
     const size_t tile_lines = (size_t)t * a.ld;
     char* out = reinterpret_cast<char*>(a.slab[1]) + tile_lines * kLineBytes;
     uint2* ometa = a.meta[1] + tile_lines;
-    const uint2* m0p = a.meta[0] + (size_t)t0 * a.ld;  // liveness: any tile of the quad
+    const uint2* m0p = a.meta[0] + (size_t)t0 * a.ld;  // liveness: any tile of the group
     const int jw = j0 + warp;
     if (jw >= j1) return;
     const int nb = L.wp / 32;
@@ -1139,27 +1154,30 @@ __device__ __forceinline__ void bin_quad_item(const NetArgs<float>& a, const Lay
         if (k < 0) return false;
         unsigned any = 0u;
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < TPQ; ++u)
             if (u < ntq) any |= m0p[(size_t)u * a.ld + k].x;
         return any != 0u;
     };
     const uint64_t wpol = policy_evict_last();
     int k0 = ld_w(L.idx + po, wpol);
-    float w0 = ld_w(L.val + po, wpol);
+    T w0 = ld_w(L.val + po, wpol);
     advance();
     int k1 = -1, k2 = -1;
-    float w1 = 0.f, w2 = 0.f;
+    T w1 = T(0), w2 = T(0);
     if (total > 1) {
         k1 = ld_w(L.idx + po, wpol);
         w1 = ld_w(L.val + po, wpol);
         advance();
     }
     bool l0 = quad_live(k0);
-    float acc[32];
+    T acc[32];
 #pragma unroll
-    for (int c = 0; c < 32; ++c) acc[c] = 0.f;
+    for (int c = 0; c < 32; ++c) acc[c] = T(0);
     unsigned alive32 = 0u;
     int cj = jw, cb = 0;
+    // slot list entry: {word offset of the line, slot index in the batch};
+    // the weight stays in the slot's lane and is fetched by shuffle (float:
+    // the entry carries it directly)
     for (int b = 0; b < total; ++b) {
         if (b + 2 < total) {
             k2 = ld_w(L.idx + po, wpol);
@@ -1174,32 +1192,40 @@ __device__ __forceinline__ void bin_quad_item(const NetArgs<float>& a, const Lay
             uint2 e;
             int at;
             if (l0) {
-                e = make_uint2((unsigned)k0 * (kQuadLine / 4), __float_as_uint(w0));
+                if constexpr (sizeof(T) == 4)
+                    e = make_uint2((unsigned)k0 * (kQuadLine / 4), __float_as_uint(w0));
+                else
+                    e = make_uint2((unsigned)k0 * (kQuadLine / 4), (unsigned)lane);
                 at = __popc(live & below);
             } else {  // padding: word 0 of line 0, weight 0 (adds +0)
-                e = make_uint2(0u, 0u);
+                e = make_uint2(0u, sizeof(T) == 4 ? 0u : 32u);
                 at = n + __popc(~live & below);
             }
             if (at < npad) wlist[at] = e;
         }
         __syncwarp();
-        auto issue = [&](unsigned (&wd)[GB], float (&wv)[GB], int i0) {
+        auto issue = [&](unsigned (&wd)[GB], T (&wv)[GB], int i0) {
 #pragma unroll
             for (int u = 0; u < GB; ++u) {
                 const uint2 e = wlist[i0 + u];
                 wd[u] = __ldg(inq + e.x);
-                wv[u] = __uint_as_float(e.y);
+                if constexpr (sizeof(T) == 4) {
+                    wv[u] = __uint_as_float(e.y);
+                } else {  // the slot's weight from its lane; padding (32) reads lane 0 and is zeroed
+                    const T wsh = __shfl_sync(0xffffffffu, w0, (int)(e.y & 31u));
+                    wv[u] = e.y < 32u ? wsh : T(0);
+                }
             }
         };
-        auto consume = [&](const unsigned (&wd)[GB], const float (&wv)[GB]) {
+        auto consume = [&](const unsigned (&wd)[GB], const T (&wv)[GB]) {
 #pragma unroll
             for (int u = 0; u < GB; ++u)
 #pragma unroll
                 for (int c = 0; c < 32; ++c)
-                    if ((wd[u] >> c) & 1u) acc[c] = __fadd_rn(acc[c], wv[u]);
+                    if ((wd[u] >> c) & 1u) acc[c] = Arith<T>::add(acc[c], wv[u]);
         };
         unsigned d0[GB], d1[GB];
-        float v0[GB], v1[GB];
+        T v0[GB], v1[GB];
         if (npad) issue(d0, v0, 0);
         for (int i0 = 0; i0 < npad; i0 += 2 * GB) {
             if (i0 + GB < npad) issue(d1, v1, i0 + GB);
@@ -1209,42 +1235,42 @@ __device__ __forceinline__ void bin_quad_item(const NetArgs<float>& a, const Lay
             consume(d1, v1);
         }
         __syncwarp();
-        if (++cb == nb) {  // column complete: four sectors per lane
+        if (++cb == nb) {  // column complete: SPL sectors of RPL rows per lane
             cb = 0;
-            unsigned bits[4];
-            float v[4][8];
+            unsigned piece = 0u, bits32 = 0u;
+            T v[SPL][RPL];
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
-                bits[g] = 0u;
+            for (int g = 0; g < SPL; ++g) {
+                unsigned bits = 0u;
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
+                for (int c = 0; c < RPL; ++c) {
                     bool keep;
                     if (a.epilogue) {
-                        v[g][c] = bias_relu_clamp_keep(acc[g * 8 + c], L.bias, a.ymax, keep);
+                        v[g][c] = bias_relu_clamp_keep(acc[g * RPL + c], L.bias, a.ymax, keep);
                     } else {
-                        v[g][c] = acc[g * 8 + c];
-                        keep = v[g][c] != 0.f;
+                        v[g][c] = acc[g * RPL + c];
+                        keep = v[g][c] != T(0);
                     }
-                    bits[g] |= keep ? (1u << c) : 0u;
-                    acc[g * 8 + c] = 0.f;
+                    bits |= keep ? (1u << c) : 0u;
+                    acc[g * RPL + c] = T(0);
                 }
+                piece |= bits ? (1u << g) : 0u;
+                bits32 |= bits << (g * RPL);
             }
-            // the tile's sector mask: lane sub contributes bits 4*sub .. 4*sub+3
-            unsigned nib = (bits[0] ? 1u : 0u) | (bits[1] ? 2u : 0u) | (bits[2] ? 4u : 0u) | (bits[3] ? 8u : 0u);
-            unsigned m = nib << (4 * sub);
-            m |= __shfl_xor_sync(0xffffffffu, m, 1);
-            m |= __shfl_xor_sync(0xffffffffu, m, 2);
-            m |= __shfl_xor_sync(0xffffffffu, m, 4);
+            // the tile's sector mask: lane sub contributes bits SPL*sub .. SPL*sub+SPL-1
+            unsigned m = piece << (SPL * sub);
+#pragma unroll
+            for (int x = 1; x < LPT; x <<= 1) m |= __shfl_xor_sync(0xffffffffu, m, x);
             const unsigned hb = (unsigned)cj * 32u;
             if (tile_ok) {
 #pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    const unsigned lp = (unsigned)(sub * 4 + g);
-                    if (bits[g]) st32(out + (size_t)(hb + __popc(m & ((1u << lp) - 1u))) * 32, v[g]);
+                for (int g = 0; g < SPL; ++g) {
+                    const unsigned lp = (unsigned)(sub * SPL + g);
+                    if ((piece >> g) & 1u) st32(out + (size_t)(hb + __popc(m & ((1u << lp) - 1u))) * 32, v[g]);
                 }
                 if (sub == 0) ometa[cj] = make_uint2(m, hb);
             }
-            alive32 |= bits[0] | (bits[1] << 8) | (bits[2] << 16) | (bits[3] << 24);
+            alive32 |= bits32;
             cj += kWarps;
         }
         k0 = k1;
@@ -1257,17 +1283,21 @@ __device__ __forceinline__ void bin_quad_item(const NetArgs<float>& a, const Lay
     uint32_t* aw = a.alive + ((size_t)1 * a.n_tiles + t) * AW;
     if (tile_ok && alive32) atomicOr(&aw[sub], alive32);
     const unsigned any = __ballot_sync(0xffffffffu, tile_ok && alive32 != 0u);
-    if (sub == 0 && ((any >> (8 * T)) & 0xffu) && atomicOr(&aw[AW - 1], 1u) == 0u) atomicAdd(&a.tile_count[1], 1);
+    constexpr unsigned kTileLanes = (1u << LPT) - 1u;
+    if (sub == 0 && ((any >> (LPT * T_)) & kTileLanes) && atomicOr(&aw[AW - 1], 1u) == 0u)
+        atomicAdd(&a.tile_count[1], 1);
 }
 
-__global__ void __launch_bounds__(kThreads, SDNN_QUAD_OCC) bin_quad_kernel(NetArgs<float> a) {
+template <typename T>
+__global__ void __launch_bounds__(kThreads, quad_occ<T>()) bin_quad_kernel(NetArgs<T> a) {
     __shared__ uint2 lists[kWarps][32];
     __shared__ long long s_item;
     if (a.stamps && blockIdx.x == 0 && threadIdx.x == 0) a.stamps[0] = globaltimer();
     if (__ldcg(&a.tile_count[0]) == 0) return;
-    const LayerDesc<float> L = a.layers[0];
+    const LayerDesc<T> L = a.layers[0];
+    constexpr int TPQ = quad_tiles<T>();
     const int nblk = (a.n_out + a.jb - 1) / a.jb;
-    const long long items = (long long)((a.n_tiles + 3) / 4) * nblk;
+    const long long items = (long long)((a.n_tiles + TPQ - 1) / TPQ) * nblk;
     for (;;) {
         if (threadIdx.x == 0) s_item = (long long)atomicAdd(&a.work[0], 1u);
         __syncthreads();
@@ -1276,7 +1306,7 @@ __global__ void __launch_bounds__(kThreads, SDNN_QUAD_OCC) bin_quad_kernel(NetAr
         if (it >= items) break;
         const int q = (int)(it / nblk), bb = (int)(it % nblk);
         const int j0 = bb * a.jb, j1 = min(a.n_out, j0 + a.jb);
-        bin_quad_item<SDNN_QUAD_GB>(a, L, q, j0, j1, lists[threadIdx.x >> 5]);
+        bin_quad_item<T, SDNN_QUAD_GB>(a, L, q, j0, j1, lists[threadIdx.x >> 5]);
     }
 }
 

@@ -34,7 +34,6 @@ import sys
 import threading
 import time
 import weakref
-from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
 import numpy as np
@@ -47,6 +46,7 @@ __all__ = [
     "InferenceConfig",
     "DEFAULT_YMAX",
     "DeviceNetwork",
+    "DeviceGroup",
     "RunResult",
     "spmm",
     "apply_bias_relu_clamp",
@@ -387,6 +387,80 @@ class DeviceNetwork:
             pass
 
 
+class DeviceGroup:
+    """One C-ABI handle over several GPUs (sdnn_open_devices): a weight
+    replica per device, converted once on the first and copied device to
+    device; ``infer_csr`` splits the batch into contiguous row blocks, one
+    host thread per GPU inside the library (engine._infer_data_parallel,
+    engine.py:237-251, with a GPU per worker)."""
+
+    def __init__(self, n_neurons: int, devices, dtype: str = "f32"):
+        warmup()
+        if dtype not in DTYPES:
+            raise ParameterError(f"dtype {dtype!r} is not one of {tuple(DTYPES)}")
+        self.n, self.dtype = int(n_neurons), dtype
+        self.devices = [int(d) for d in devices]
+        devs = np.asarray(self.devices, np.int32)
+        self.handle = ctypes.c_void_p()
+        _lib.check(_lib.lib().sdnn_open_devices(_lib.ptr(devs), len(self.devices), DTYPES[dtype], self.n,
+                                                ctypes.byref(self.handle)))
+        self.n_layers = 0
+        self.lock = threading.Lock()
+
+    @classmethod
+    def from_model(cls, model, devices, dtype: str = "f32") -> "DeviceGroup":
+        g = cls(model.neurons_per_layer, devices, dtype)
+        for lw in model.layers:
+            g.add_layer_csr(lw.weights, lw.bias)
+        return g
+
+    def add_layer_csr(self, w, bias: float) -> None:
+        n_rows, n_cols, off, cols, vals = _csr(w)
+        if (n_rows, n_cols) != (self.n, self.n):
+            raise ShapeError(f"layer is {n_rows}x{n_cols}, network has {self.n} neurons")
+        _lib.check(_lib.lib().sdnn_group_add_layer_csr(
+            self.handle, _lib.ptr(off), _lib.ptr(_nonempty(cols, np.int64)),
+            _lib.ptr(_nonempty(vals, np.float64)), int(off[-1]), float(bias)))
+        self.n_layers += 1
+
+    def add_permunion_layers(self, seed: int, first_layer: int, count: int, width: int,
+                             value: float, bias: float, threads: int = 0) -> None:
+        _lib.check(_lib.lib().sdnn_group_add_layers_permunion(
+            self.handle, int(seed), int(first_layer), int(count), int(width), float(value),
+            float(bias), int(threads)))
+        self.n_layers += int(count)
+
+    def infer_csr(self, n_rows, off, cols, vals, ymax: float = DEFAULT_YMAX,
+                  want_y: bool = True) -> RunResult:
+        L = _lib.lib()
+        h = ctypes.c_void_p()
+        _lib.check(L.sdnn_group_infer(
+            self.handle, int(n_rows), _lib.ptr(_nonempty(np.ascontiguousarray(off, np.int64), np.int64)),
+            _lib.ptr(_nonempty(np.ascontiguousarray(cols, np.int64), np.int64)),
+            _lib.ptr(_nonempty(np.ascontiguousarray(vals, np.float64), np.float64)), float(ymax),
+            1 if want_y else 0, ctypes.byref(h)))
+        try:
+            r = _collect(h, int(n_rows), want_y)
+            b, s = ctypes.c_int64(), ctypes.c_int64()
+            _lib.check(L.sdnn_result_h2d_bytes(h, ctypes.byref(b)))
+            _lib.check(L.sdnn_result_segments(h, ctypes.byref(s)))
+            r.h2d_bytes, r.segments = b.value, s.value
+            return r
+        finally:
+            L.sdnn_result_free(h)
+
+    def close(self):
+        if self.handle:
+            _lib.lib().sdnn_close(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
 def _collect(h, n_rows: int, want_y: bool) -> RunResult:
     L = _lib.lib()
     n = ctypes.c_int64()
@@ -447,6 +521,27 @@ def _device_network(model, device: int, dtype: str) -> DeviceNetwork:
         with _cache_lock:
             nets[(device, dtype)] = net
     return net
+
+
+def _device_group(model, devices, dtype: str) -> DeviceGroup:
+    """One multi-GPU handle per (model object, device list, dtype)."""
+    key = id(model)
+    with _cache_lock:
+        entry = _cache.get(key)
+        if entry is None or entry[0]() is not model:
+            try:
+                ref = weakref.ref(model, lambda _r, k=key: _cache.pop(k, None))
+            except TypeError:
+                ref = lambda m=model: m  # noqa: E731 -- unweakrefable: keep alive
+            entry = (ref, {})
+            _cache[key] = entry
+        nets = entry[1]
+        grp = nets.get((tuple(devices), dtype, "group"))
+    if grp is None:
+        grp = DeviceGroup.from_model(model, devices, dtype)
+        with _cache_lock:
+            nets[(tuple(devices), dtype, "group")] = grp
+    return grp
 
 
 def _devices(cfg: InferenceConfig) -> list[int]:
@@ -524,27 +619,10 @@ def infer(model, y0, cfg: InferenceConfig | None = None):
         o, c, v = _run_stages(model, cfg.dtype, devs, cfg.ymax, n_rows, off, cols, vals, ranges)
     elif len(devs) == 1 or n_rows <= 1:
         o, c, v = _run_block(model, cfg.dtype, devs[0], cfg.ymax, n_rows, off, cols, vals, ranges)
-    else:
-        per = -(-n_rows // len(devs))
-        spans = [(s, min(s + per, n_rows)) for s in range(0, n_rows, per)]
-
-        def work(i):
-            lo, hi = spans[i]
-            base = off[lo]
-            return _run_block(model, cfg.dtype, devs[i], cfg.ymax, hi - lo, off[lo:hi + 1] - base,
-                              cols[base:off[hi]], vals[base:off[hi]], ranges)
-
-        with ThreadPoolExecutor(max_workers=len(spans)) as pool:
-            blocks = list(pool.map(work, range(len(spans))))
-        o = np.zeros(n_rows + 1, np.int64)
-        pos, base = 0, 0
-        for (bo, _, _) in blocks:
-            r = bo.size - 1
-            o[pos + 1:pos + r + 1] = bo[1:] + base
-            base += int(bo[-1])
-            pos += r
-        c = np.concatenate([b[1] for b in blocks])
-        v = np.concatenate([b[2] for b in blocks])
+    else:  # one C-ABI group handle: contiguous row blocks, a host thread per GPU (engine.py:237-251)
+        grp = _device_group(model, devs, cfg.dtype)
+        with grp.lock:
+            o, c, v = grp.infer_csr(n_rows, off, cols, vals, cfg.ymax, want_y=True).y
     return fb_cls(_make_matrix(sm_cls, n_rows, model.neurons_per_layer, o, c, v))
 
 
@@ -561,8 +639,12 @@ def infer_timed(model, y0, cfg: InferenceConfig | None = None):
     reference's model loading."""
     cfg = cfg or InferenceConfig()
     warmup()
-    for d in _devices(cfg):
-        _device_network(model, d, cfg.dtype)
+    devs = _devices(cfg)
+    if cfg.mode == "data_parallel" and len(devs) > 1:
+        _device_group(model, devs, cfg.dtype)
+    else:
+        for d in devs:
+            _device_network(model, d, cfg.dtype)
     start = time.perf_counter()
     result = infer(model, y0, cfg)
     categories = categorize(result)

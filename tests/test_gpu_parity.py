@@ -15,6 +15,7 @@ import numpy as np
 import pytest
 
 import goldens
+from parity import assert_f32_within
 from oracle import oracle as O
 
 pytestmark = pytest.mark.gpu
@@ -92,16 +93,30 @@ def test_general_goldens_f32_is_the_oracle_float_instance():
 
 
 def test_radixnet_digits_f64_bit_exact_and_f32_tolerance():
+    """The reference's own acceptance workload (RadiX-Net 1024 + synthetic
+    digits, golden from the reference).  float64: bit-exact.  float32: the
+    oracle's float instance bit for bit, the same stored pattern and
+    categories as the reference at 24 and 120 layers, and the final Y within
+    the stated tolerance.  At 120 layers every survivor has saturated, so
+    float32 meets north_star's 1e-5.  At 24 layers the values are in their
+    unsaturated transient, where a bias of -0.3 against sums near 0.3
+    cancels most significant bits: float32 then carries up to 0.59 relative
+    error on 0.4 % of the entries (measured with the oracle's float
+    instance, which our float32 path equals bit for bit), so this depth is
+    outside the 1e-5 contract and the float64 path is the one to use."""
     r = goldens.radixnet()
-    for L, y, cats in ((24, r["y24"], r["cats24"]), (120, r["y120"], r["cats120"])):
+    for L, y, cats, rtol in ((24, r["y24"], r["cats24"], 0.6), (120, r["y120"], r["cats120"], 1e-5)):
         model = model_of(r["layers"][:L], r["bias"][:L], r["n"])
         out = E.infer(model, FeatureBatch(sm(r["y0"])))
         assert as_csr(out).identical(y)
         out32 = E.infer(model, FeatureBatch(sm(r["y0"])), E.InferenceConfig(dtype="f32"))
         want32 = O.infer(r["layers"][:L], r["bias"][:L], r["y0"], precision=32)
         assert as_csr(out32).identical(want32)
-        # categories survive float32 on this workload (values saturate or die)
         assert np.array_equal(O.categorize(as_csr(out32)), cats)
+        worst = assert_f32_within(as_csr(out32), y, rtol)
+        if L == 24:
+            rel = np.abs(as_csr(out32).vals - y.vals) / np.abs(y.vals)
+            assert (rel > 1e-5).mean() < 0.01 and worst > 1e-5
 
 
 # -------------------------------------------------------------- KATs on GPU
@@ -436,26 +451,8 @@ def test_streamed_e2e_empty_batch_and_bad_input():
     net.close()
 
 
-# ------------------------------------------------ BASELINE configs, full size
-
-def test_c1_as_specified_full_size():
-    """C1 (N=1024, L=120, 60,000 rows) in full against the oracle; the
-    category list must be bit-exact in both precisions."""
-    w = W.CONFIGS["C1"]
-    off, cols, vals = W.images(w)
-    y0 = O.CSR(w.batch, w.n, off, cols, vals)
-    layers = [O.CSR(w.n, w.n, *c) for c in W.layers_csr(w)]
-    want = O.infer(layers, [w.bias] * w.layers, y0, threads=os.cpu_count() or 8)
-    for dtype in ("f32", "f64"):
-        net = E.DeviceNetwork(w.n, 0, dtype)
-        net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias)
-        res = net.run(net.upload_csr(w.batch, off, cols, vals), w.ymax, want_y=True)
-        assert np.array_equal(res.categories, O.categorize(want)), dtype
-        assert O.CSR(w.batch, w.n, *res.y).nnz == want.nnz
-        if dtype == "f64":
-            assert O.CSR(w.batch, w.n, *res.y).identical(want)
-        net.close()
-
+# ------------------------------------------------ flagship width, full batch
+# (the BASELINE configs as specified: tests/test_gpu_configs.py)
 
 def test_c4_shape_full_batch_row_sample_consistency():
     """Flagship width at full batch: rows are independent, so a 64-row
@@ -479,55 +476,6 @@ def test_c4_shape_full_batch_row_sample_consistency():
     want = O.infer(layers, [w.bias] * w.layers, O.CSR(64, w.n, s_off, s_cols, s_vals),
                    precision=32, threads=os.cpu_count() or 8)
     assert O.CSR(64, w.n, *part.y).identical(want)
-
-
-def _oracle_rows(w, rows, precision):
-    """Oracle over the first `rows` rows of workload w (all layers)."""
-    off, cols, vals = W.images(w, n_rows=rows)
-    layers = [O.CSR(w.n, w.n, *c) for c in W.layers_csr(w)]
-    return O.infer(layers, [w.bias] * w.layers, O.CSR(rows, w.n, off, cols, vals), w.ymax,
-                   precision=precision, threads=os.cpu_count() or 8)
-
-
-@pytest.mark.parametrize("name", ["C2", "C3"])
-def test_c2_c3_as_specified_full_batch(name):
-    """C2 (N=4096, L=480) and C3 (N=16384, L=1920) over all 60,000 rows on
-    the GPU; categories and live-row counts checked against the oracle on a
-    3,000-row prefix (rows are independent), f32 and f64."""
-    w = W.CONFIGS[name]
-    off, cols, vals = W.images(w)
-    want64 = _oracle_rows(w, 3000, 64)
-    for dtype in ("f32", "f64"):
-        net = E.DeviceNetwork(w.n, 0, dtype)
-        net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias)
-        full = net.run(net.upload_csr(w.batch, off, cols, vals), w.ymax)
-        assert full.live_rows[0] == np.count_nonzero(np.diff(off))
-        head = net.run(net.upload_csr(3000, off[:3001], cols[:off[3000]], vals[:off[3000]]), w.ymax,
-                       want_y=True)
-        if dtype == "f64":
-            assert O.CSR(3000, w.n, *head.y).identical(want64)
-        assert np.array_equal(head.categories, O.categorize(want64))
-        assert np.array_equal(full.categories[full.categories <= 3000], head.categories)
-        net.close()
-
-
-@pytest.mark.parametrize("batch,p", [(1000, 0.1), (15000, 0.35), (60000, 0.7), (240000, 0.7)])
-def test_c5_sweep_cells(batch, p):
-    """C5 sweep cells (N=65536, L=120): full batch on the GPU, oracle on a
-    400-row prefix; categories and the prefix's final Y must agree."""
-    w = W.CONFIGS["C5"].with_(batch=batch, p=p)
-    off, cols, vals = W.images(w)
-    net = E.DeviceNetwork(w.n, 0, "f32")
-    net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias)
-    full = net.run(net.upload_csr(w.batch, off, cols, vals), w.ymax)
-    assert full.live_rows[0] == np.count_nonzero(np.diff(off))
-    rows = min(400, batch)
-    want = _oracle_rows(w, rows, 32)
-    head = net.run(net.upload_csr(rows, off[:rows + 1], cols[:off[rows]], vals[:off[rows]]), w.ymax,
-                   want_y=True)
-    assert O.CSR(rows, w.n, *head.y).identical(want)
-    assert np.array_equal(full.categories[full.categories <= rows], O.categorize(want))
-    net.close()
 
 
 @pytest.mark.parametrize("dtype,prec", [("f64", 64), ("f32", 32)])
@@ -719,3 +667,34 @@ def test_images_to_categories_on_device(dtype, prec):
     assert O.CSR(y0.n_rows, w.n, *res.y).identical(want)
     assert np.array_equal(res.categories, O.categorize(want))
     net.close()
+
+
+# ------------------------------------------- multi-GPU handle (C ABI group)
+
+@pytest.mark.parametrize("devices", [(0,), (0, 0), (0, 0, 0)])
+@pytest.mark.parametrize("dtype,prec", [("f64", 64), ("f32", 32)])
+def test_group_handle_matches_one_gpu(devices, dtype, prec):
+    """sdnn_open_devices / sdnn_group_*: weights converted on the first
+    member and copied device to device, the batch split into ceil(B/G)-row
+    blocks run concurrently from one host thread per member, merged in row
+    order: bit-identical to the oracle (and so to one GPU), with the
+    categories shifted by each block's first row."""
+    w, y0, layers = permunion_case(1024, 6, 517, 0.125)
+    g = E.DeviceGroup(w.n, devices, dtype)
+    for l in range(w.layers):
+        g.add_layer_csr(sm(layers[l]), w.bias)
+    res = g.infer_csr(y0.n_rows, y0.off, y0.cols, y0.vals, w.ymax, want_y=True)
+    want = O.infer(layers, [w.bias] * w.layers, y0, precision=prec, threads=4)
+    assert O.CSR(y0.n_rows, w.n, *res.y).identical(want)
+    assert np.array_equal(res.categories, O.categorize(want))
+    assert res.live_rows[0] == np.count_nonzero(np.diff(y0.off))
+    r2 = g.infer_csr(y0.n_rows, y0.off, y0.cols, y0.vals, w.ymax, want_y=False)
+    assert np.array_equal(r2.categories, res.categories)
+    g.close()
+    g = E.DeviceGroup(w.n, devices, dtype)  # perm-union layers generated once, replicated
+    g.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias)
+    r3 = g.infer_csr(y0.n_rows, y0.off, y0.cols, y0.vals, w.ymax, want_y=True)
+    assert O.CSR(y0.n_rows, w.n, *r3.y).identical(want)
+    empty = g.infer_csr(0, np.zeros(1, np.int64), np.zeros(0, np.int64), np.zeros(0), w.ymax)
+    assert empty.categories.size == 0
+    g.close()
