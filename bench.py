@@ -327,6 +327,12 @@ class DeviceArm:
         threads = host_threads()
         self.net = net = DeviceNetwork(w.n, self.device, args.dtype)
         weights = args.weights if args.weights != "auto" else ("broadcast" if dist.world > 1 else "generate")
+        if w.kind == "radixnet":  # K1: RadiX-Net weights, digit-like images resized on the device
+            net.add_radixnet_layers(w.weight_seed, 0, w.layers, w.value, w.bias)
+            self.batch = net.upload_images(W.stroke_images(w.batch)[r0:r1], w.side)
+            self.off, self.cols, self.vals = self.batch.to_csr()
+            self.nnz0 = int(self.off[-1])
+            return
         if weights == "broadcast" and dist.world > 1:
             if dist.rank == 0:
                 net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias,
@@ -534,7 +540,7 @@ def run_ours(args, dist: RankGroup, arm_cls=None):
             line["f64"] = f64_line(args, w)
         if args.companions:
             line["companions"] = companions(args)
-    if dist.rank == 0 and dist.world == 1 and not args.no_cpu:
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu and w.kind == "permunion":
         line["cpu_baseline"] = cpu_baseline(w, args.cpu_rows)
     return line
 
@@ -618,9 +624,17 @@ def companions(args):
         if L:
             w = w.with_(layers=int(L))
         net = DeviceNetwork(w.n, 0, args.dtype)
-        net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias)
-        off, cols, vals = W.images(w)
-        b = net.upload_csr(w.batch, off, cols, vals)
+        t_setup = time.perf_counter()
+        if w.kind == "radixnet":  # K1: RadiX-Net weights, digit-like images resized on the device
+            net.add_radixnet_layers(w.weight_seed, 0, w.layers, w.value, w.bias)
+            b = net.upload_images(W.stroke_images(w.batch), w.side)
+            nnz0 = b.nnz()
+        else:
+            net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias)
+            off, cols, vals = W.images(w)
+            b = net.upload_csr(w.batch, off, cols, vals)
+            nnz0 = int(off[-1])
+        setup_s = time.perf_counter() - t_setup
         for _ in range(2):
             net.run(b, w.ymax)
         steps = 3
@@ -636,12 +650,16 @@ def companions(args):
         net.set_layer_timing(True)
         p = net.run(b, w.ymax)
         elem = 8 if args.dtype == "f64" else 4
-        lb = layer_bytes(w, elem, p.live_rows, int(off[-1]), w.batch)
+        lb = layer_bytes(w, elem, p.live_rows, nnz0, w.batch)
         peak, _ = hbm_peak()
         mid = w.layers // 2
         gbs = lb[mid] / (p.layer_ms[mid] * 1e-3) / 1e9 if p.layer_ms[mid] > 0 else 0.0
         out.append({
-            "workload": f"{w.name}: N={w.n}, L={w.layers}, batch={w.batch}, w={w.value}",
+            "workload": (f"{w.name}: N={w.n}, L={w.layers}, batch={w.batch}, w={w.value}, bias={w.bias}, "
+                         + ("RadiX-Net preset seed 42 (radixnet.py:293-310), 28x28 digit-like images "
+                            "resized to 256x256 on the device" if w.kind == "radixnet"
+                            else f"perm-union weights, Bernoulli({w.p}) images")),
+            "setup_s": setup_s,
             "value": w.edges / (ms * 1e-3),
             "ms_per_step": ms,
             "steps": steps,
@@ -763,7 +781,7 @@ def parser():
     ap.add_argument("--also-f64", dest="also_f64", action="store_true", default=None,
                     help="N=1, f32: add the workload on the float64 path (default for C4)")
     ap.add_argument("--no-f64", dest="also_f64", action="store_false")
-    ap.add_argument("--companions", default="K2:120",
+    ap.add_argument("--companions", default="K2:120,K1",
                     help="comma list NAME[:LAYERS] of live companions ('' to skip)")
     return ap
 

@@ -681,6 +681,11 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     // left in 4 tiles, repacking them cost more than it saved)
     a.compact_min = std::max(1, env_int("SDNN_COMPACT_MIN", 16));
     a.jb = env_int("SDNN_JB", net->jb);
+    // dense inputs (>= 60 % of sectors kept): 64-output items -- measured on
+    // the K2 companion's dense layers, 36.7 -> 29.9 ms at JB 256 -> 64; C4's
+    // 34 %-dense layer 2 is fastest at 256 (17.7 vs 18.3 ms at 64)
+    a.jb_dense = env_int("SDNN_JB_DENSE", 64);
+    a.dense_pct = env_int("SDNN_DENSE_PCT", 60);
     const int kc = std::min(1024, env_int("SDNN_DENSIFY_KC", 96));  // input neurons per staging chunk
     const size_t dsmem = (size_t)kc * kLineBytes;
     const void* dfn = (const void*)densify_kernel<T>;

@@ -252,7 +252,14 @@ struct NetArgs {
     int compact_pct;      // repack when >= this % of the live tiles would be freed (<= 0: never)
     int compact_min;      // ... and at least this many tiles (a repack costs a pass and a grid barrier)
     int* n_compact;       // compactions done (written by block 0 at the end)
+    // density-adaptive work items: a layer takes jb_dense-output items
+    // instead of jb when a fixed sample of its input lines is at least
+    // dense_pct % sectors-dense (a dense 256-row tile is 64 MB of lines: a
+    // narrower item window keeps the tile being gathered inside L2)
+    int jb_dense;
+    int dense_pct;
 };
+constexpr int kDensitySample = 256;  // input lines sampled per layer (the same ones in every CTA)
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
@@ -990,6 +997,8 @@ struct LayerShared {
     int count;
     int scan[kWarps + 1];
     long long item;
+    long long items;  // work items of the current layer
+    int jb, nblk;     // outputs per item, items per tile
 };
 
 // One layer for this CTA: build the ascending live-tile list from the
@@ -1026,8 +1035,33 @@ __device__ __forceinline__ void layer_pass(const NetArgs<T>& a, int l, int32_t* 
     }
     const int count = sh.count;
     const LayerDesc<T> L = a.layers[l];
-    const int nblk = (a.n_out + a.jb - 1) / a.jb;
-    const long long items = (long long)((count + TP - 1) / TP) * nblk;
+    int jb_l = a.jb;
+    if (a.jb_dense > 0 && a.jb_dense != a.jb && !BIN && count > 0) {
+        // the input's sector density picks the item width: every CTA samples
+        // the same kDensitySample (tile, line) metas, so all decide alike
+        const uint2* imeta = odd ? a.meta[1] : a.meta[0];
+        unsigned c = 0u;
+        for (int i = tid; i < kDensitySample; i += kThreads) {
+            const int t = tiles[(int)(((unsigned)i * 2654435761u) % (unsigned)count)];
+            const int k = (int)(((unsigned)i * 40503u + 17u) % (unsigned)a.n_in);
+            c += (unsigned)__popc(__ldcg(&imeta[(size_t)t * a.ld + k]).x);
+        }
+        for (int x = 16; x > 0; x >>= 1) c += __shfl_xor_sync(0xffffffffu, c, x);
+        if (lane == 0) sh.scan[warp] = (int)c;
+        __syncthreads();
+        int tot = 0;
+        for (int w = 0; w < kWarps; ++w) tot += sh.scan[w];
+        __syncthreads();
+        if ((long long)tot * 100 >= (long long)a.dense_pct * kDensitySample * 32) jb_l = a.jb_dense;
+    }
+    // the item width and item count live in shared memory, not in registers
+    // across the item loop (the gather loop needs every register it has)
+    if (tid == 0) {
+        sh.jb = jb_l;
+        sh.nblk = (a.n_out + jb_l - 1) / jb_l;
+        sh.items = (long long)((count + TP - 1) / TP) * sh.nblk;
+    }
+    __syncthreads();
     // items are handed out in order from a counter, so all CTAs work on a
     // narrow window of tiles and the tiles' input lines stay in L2 across
     // the 32 columns that gather each of them
@@ -1035,11 +1069,13 @@ __device__ __forceinline__ void layer_pass(const NetArgs<T>& a, int l, int32_t* 
         if (tid == 0) sh.item = (long long)atomicAdd(&a.work[l], 1u);
         __syncthreads();
         const long long it = sh.item;
+        const int jb = sh.jb, nblk = sh.nblk;
+        const bool done = it >= sh.items;
         __syncthreads();
-        if (it >= items) break;
+        if (done) break;
         const int ti = (int)(it / nblk) * TP;
         const int bb = (int)(it % nblk);
-        const int j0 = bb * a.jb, j1 = min(a.n_out, j0 + a.jb);
+        const int j0 = bb * jb, j1 = min(a.n_out, j0 + jb);
         if constexpr (TP == 2 && BIN && sizeof(T) == 4) {
             bin_item2<GB>(a, L, tiles[ti], ti + 1 < count ? tiles[ti + 1] : -1, j0, j1,
                           reinterpret_cast<BinEntry2*>(sh.list[warp]));

@@ -176,6 +176,11 @@ class DeviceBatch:
         self.h2d_bytes = b.value
         net._batches.add(self)  # freed before the network that owns its stream
 
+    def nnz(self) -> int:
+        n = ctypes.c_int64()
+        _lib.check(_lib.lib().sdnn_batch_nnz(self.handle, ctypes.byref(n)))
+        return n.value
+
     def to_csr(self):
         """(off, cols, vals) of the staged batch, int64/int64/float64."""
         L = _lib.lib()
@@ -256,6 +261,20 @@ class DeviceNetwork:
             self.handle, int(seed), int(first_layer), int(count), int(width), float(value),
             float(bias), int(threads)))
         self.n_layers += int(count)
+
+    def add_radixnet_layers(self, seed: int, first_layer: int, count: int, value: float, bias: float,
+                            chunk: int = 32) -> None:
+        """Append layers [first_layer, first_layer + count) of the RadiX-Net
+        preset network over this width (the reference's own generator,
+        radixnet.py:293-310, restated in workloads.radixnet_ell), every
+        slot holding `value`."""
+        from . import workloads as W
+
+        vals = np.full(self.n * 32, float(value), np.float64)
+        for l0 in range(first_layer, first_layer + count, chunk):
+            m = min(chunk, first_layer + count - l0)
+            for idx in W.radixnet_ell_layers(self.n, l0, m, seed):
+                self.add_layer_ell(idx, vals, bias)
 
     def add_layers_uninit(self, count: int, width: int, bias: float) -> None:
         """Append `count` layers whose device buffers the caller fills (the

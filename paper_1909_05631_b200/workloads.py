@@ -40,6 +40,7 @@ class Workload:
     ymax: float = 32.0
     weight_seed: int = WEIGHT_SEED
     image_seed: int = IMAGE_SEED
+    kind: str = "permunion"  # weights: "permunion" (BASELINE generator) or "radixnet" (K1)
 
     @property
     def edges(self) -> int:
@@ -57,8 +58,60 @@ CONFIGS = {
     "C4": Workload("C4", 65536, 1920, 60000, 256, 160, 0.35, -0.45),
     "C5": Workload("C5", 65536, 120, 60000, 256, 160, 0.35, -0.45),
     "K2": Workload("K2", 65536, 1920, 60000, 256, 160, 0.35, -0.45, value=0.125),
+    # K1: the reference's own workload shape at flagship width -- RadiX-Net
+    # preset (65536, 1920) seed 42 and digit-like 28x28 images resized to
+    # 256x256 on the device (stroke_images; rows stay alive and saturate).
+    # A 6,000-row sample of the 60,000-image batch.
+    "K1": Workload("K1", 65536, 1920, 6000, 256, 0, 0.0, -0.45, weight_seed=42, kind="radixnet"),
 }
 C5_SWEEP = [(b, p) for b in (1000, 15000, 60000, 240000) for p in (0.1, 0.35, 0.7)]
+
+
+# ------------------------------------------------------------- RadiX-Net (K1)
+# The reference's own network family (sdnnbench.radixnet): a radix-2
+# butterfly base of S stages over n/16 neurons (stage s links i with
+# i XOR 2^s, radixnet.py:148-175), each stage Kronecker-expanded by the
+# 16 x 16 all-ones block (radixnet.py:178-208: 32 inputs per neuron), and
+# layer t the base stage (t-1) mod S conjugated by seeded neuron
+# relabelings on both sides (perm_{t-1} on inputs, perm_t on outputs,
+# perm_0 = identity; radixnet.py:246-268,293-310).  perm_t is a uniform
+# permutation from numpy's counter-based Philox stream keyed (seed, t)
+# (radixnet.py:192-196), so any layer is produced alone, in any order.
+RADIX_PRESETS = {1024: (6, 16), 4096: (8, 16), 16384: (10, 16), 65536: (12, 16)}  # radixnet.py:46-51
+RADIX_BIAS = {1024: -0.30, 4096: -0.35, 16384: -0.40, 65536: -0.45}  # radixnet.py:39
+RADIX_SEED = 42  # the reference's acceptance workload seed
+
+
+def radix_perm(seed: int, t: int, n: int) -> np.ndarray:
+    key = np.array([seed & 0xFFFFFFFFFFFFFFFF, t], dtype=np.uint64)
+    return np.random.Generator(np.random.Philox(key=key)).permutation(n).astype(np.int64)
+
+
+def radixnet_ell(n: int, layer: int, seed: int = RADIX_SEED) -> np.ndarray:
+    """Layer `layer` (0-based; depth slot t = layer + 1) of the RadiX-Net
+    preset network over n neurons as ELL by output column: [n][32] int32,
+    the 32 inputs of each output ascending."""
+    stages, k = RADIX_PRESETS[n]
+    t = layer + 1
+    place = 1 << ((t - 1) % stages)
+    cur = radix_perm(seed, t, n)
+    inv = np.empty(n, np.int64)
+    inv[cur] = np.arange(n, dtype=np.int64)    # output j' is expanded-stage neuron inv[j']
+    i = inv // k                               # its base-butterfly neuron
+    base = np.stack([i & ~place, i | place], axis=1)  # the stage's two partners (symmetric)
+    inputs = (base[:, :, None] * k + np.arange(k, dtype=np.int64)[None, None, :]).reshape(n, 2 * k)
+    if t > 1:
+        inputs = radix_perm(seed, t - 1, n)[inputs]
+    inputs.sort(axis=1)
+    return inputs.astype(np.int32)
+
+
+def radixnet_ell_layers(n: int, first: int, count: int, seed: int = RADIX_SEED,
+                        threads: int | None = None) -> list:
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=threads or _threads()) as pool:
+        return list(pool.map(lambda l: radixnet_ell(n, l, seed), range(first, first + count)))
 
 
 def _threads() -> int:

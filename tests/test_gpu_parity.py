@@ -698,3 +698,44 @@ def test_group_handle_matches_one_gpu(devices, dtype, prec):
     empty = g.infer_csr(0, np.zeros(1, np.int64), np.zeros(0, np.int64), np.zeros(0), w.ymax)
     assert empty.categories.size == 0
     g.close()
+
+
+# ------------------------------------ K1: RadiX-Net at flagship width (65536)
+
+@pytest.mark.parametrize("dtype,prec", [("f64", 64), ("f32", 32)])
+def test_k1_radixnet_flagship_width(dtype, prec):
+    """The reference's own network family at N=65536 (RadiX-Net preset,
+    seed 42, weights pinned to the reference generator by
+    tests/test_workloads.py) fed digit-like images resized to 256x256 on
+    the device: 24 rows through 24 layers against the oracle's same
+    precision instance (float64 = the reference's arithmetic), via both
+    the device ingest and the host CSR."""
+    n, L, rows = 65536, 24, 24
+    w = W.CONFIGS["K1"].with_(layers=L, batch=rows)
+    pix = W.stroke_images(rows)
+    y0 = O.resize_threshold_flatten(pix, 256)
+    layers = [O.CSR(n, n, *c) for c in
+              (_ell_csr(W.radixnet_ell(n, l), n, w.value) for l in range(L))]
+    want = O.infer(layers, [w.bias] * L, y0, precision=prec, threads=os.cpu_count() or 8)
+    assert want.nnz > 0
+    net = E.DeviceNetwork(n, 0, dtype)
+    net.add_radixnet_layers(w.weight_seed, 0, L, w.value, w.bias)
+    b = net.upload_images(pix, 256)
+    off, cols, vals = b.to_csr()
+    assert np.array_equal(off, y0.off) and np.array_equal(cols, y0.cols)
+    res = net.run(b, w.ymax, want_y=True)
+    assert O.CSR(rows, n, *res.y).identical(want)
+    res2 = net.run(net.upload_csr(rows, y0.off, y0.cols, y0.vals), w.ymax, want_y=True)
+    assert O.CSR(rows, n, *res2.y).identical(want)
+    net.close()
+
+
+def _ell_csr(idx, n, value):
+    from paper_1909_05631_b200 import _lib
+    off = np.zeros(n + 1, np.int64)
+    cols = np.zeros(idx.size, np.int64)
+    vals = np.zeros(idx.size)
+    _lib.check_gen(_lib.gen().sdnn_gen_ell_to_csr(n, n, idx.shape[1], _lib.ptr(idx),
+                                                  _lib.ptr(np.full(idx.size, value)), _lib.ptr(off),
+                                                  _lib.ptr(cols), _lib.ptr(vals)))
+    return off, cols, vals
