@@ -707,17 +707,19 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     occ = std::min(occ, std::max(1, env_int("SDNN_OCC", occ)));
     const int grid = net->sm_count * occ;
     void* args[] = {(void*)&a};
-    bool quad = false;  // layer 1 over quad bit-lines (binary Y0, float)
+    bool quad = false;  // layer 1 over quad (float) / oct (double) bit-lines
     if (n_tiles) {
+        const bool bin = batch->vals == nullptr && env_int("SDNN_BIN", 1) != 0;
+        quad = bin && env_int("SDNN_QUAD", 1) != 0;
+        constexpr int TPQ = quad_tiles<T>();
         // lines densify does not touch stay {mask 0}: zero the meta first
-        CK(cudaMemsetAsync(a.meta[0], 0, (size_t)n_tiles * ld * sizeof(uint2), net->stream));
+        // (quad mode: one liveness word per (tile group, line))
+        const int64_t meta_rows = quad ? (n_tiles + TPQ - 1) / TPQ : n_tiles;
+        CK(cudaMemsetAsync(a.meta[0], 0, (size_t)meta_rows * ld * sizeof(uint2), net->stream));
         // each tile's neurons are split into spans handled by separate blocks
         const int spans = std::max(1, env_int("SDNN_DENSIFY_SPANS", 16));
-        const bool bin = batch->vals == nullptr && env_int("SDNN_BIN", 1) != 0;
         a.bin_in = bin ? 1 : 0;
         if (bin) {  // binary Y0: bit-line tiles
-            quad = env_int("SDNN_QUAD", 1) != 0;
-            constexpr int TPQ = quad_tiles<T>();
             if (quad)  // group lines of dead neurons / missing tiles must read as zero
                 CK(cudaMemsetAsync(a.slab[0], 0, (size_t)((n_tiles + TPQ - 1) / TPQ) * ld * kQuadLine,
                                    net->stream));

@@ -569,7 +569,9 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_bin_kernel(const int6
                                                           (t % TPQ) * (W * 4));
                     dst[0] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
                     if (W == 8) dst[1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
-                    gm[k0 + k] = make_uint2(0xFFFFFFFFu, (unsigned)(k0 + k));
+                    // one liveness word per (group, line): every tile of the
+                    // group that holds the line writes the same value
+                    meta0[(size_t)(t / TPQ) * ld + (k0 + k)] = make_uint2(0xFFFFFFFFu, (unsigned)(k0 + k));
                 } else if (any) {
                     const unsigned base = atomicAdd(&heap0[t], 1u);
                     uint4* dst = reinterpret_cast<uint4*>(s0 + (size_t)base * 32);
@@ -1165,7 +1167,7 @@ __device__ __forceinline__ void bin_quad_item(const NetArgs<T>& a, const LayerDe
     const size_t tile_lines = (size_t)t * a.ld;
     char* out = reinterpret_cast<char*>(a.slab[1]) + tile_lines * kLineBytes;
     uint2* ometa = a.meta[1] + tile_lines;
-    const uint2* m0p = a.meta[0] + (size_t)t0 * a.ld;  // liveness: any tile of the group
+    const uint2* m0p = a.meta[0] + (size_t)q * a.ld;  // liveness of the group's lines (densify, quad mode)
     const int jw = j0 + warp;
     if (jw >= j1) return;
     const int nb = L.wp / 32;
@@ -1186,14 +1188,7 @@ __device__ __forceinline__ void bin_quad_item(const NetArgs<T>& a, const LayerDe
             po += col_skip;
         }
     };
-    auto quad_live = [&](int k) -> bool {
-        if (k < 0) return false;
-        unsigned any = 0u;
-#pragma unroll
-        for (int u = 0; u < TPQ; ++u)
-            if (u < ntq) any |= m0p[(size_t)u * a.ld + k].x;
-        return any != 0u;
-    };
+    auto quad_live = [&](int k) -> bool { return k >= 0 && m0p[k].x != 0u; };
     const uint64_t wpol = policy_evict_last();
     int k0 = ld_w(L.idx + po, wpol);
     T w0 = ld_w(L.val + po, wpol);
