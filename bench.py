@@ -368,8 +368,14 @@ class DeviceArm:
         # covers layer 1, the persistent launch the rest
         stage_ms = dist.max_array(self.stage_ms / steps)
         bin_first = stage_ms[1] > 0
-        launch_bytes = [0.0, float(lb[0]) if bin_first else 0.0, float(lb[1:].sum() if bin_first else lb.sum())]
-        names = ["densify_kernel (Y0 -> tiles)", "bin_layer_kernel (layer 1, bit-line tiles)",
+        # the Y0 CSR read of layer 1's byte model happens in the densify launch
+        # (bit-line tiles); the first-layer launch keeps the output write and
+        # the weights
+        rd0 = float(self.nnz0 * (4 + elem) + (self.rows + 1) * 8) if prof.live_rows[0] > 0 else 0.0
+        launch_bytes = [rd0 if bin_first else 0.0, float(lb[0]) - rd0 if bin_first else 0.0,
+                        float(lb[1:].sum() if bin_first else lb.sum())]
+        names = ["densify_bin_kernel (Y0 -> bit-line tiles)" if bin_first else "densify_kernel (Y0 -> tiles)",
+                 "bin_quad_kernel (layer 1, quad/oct bit-lines)",
                  f"net_kernel (layers {2 if bin_first else 1}-{w.layers}, persistent)"]
         dom = int(np.argmax(stage_ms))
         dom_gbs = launch_bytes[dom] / (stage_ms[dom] * 1e-3) / 1e9 if stage_ms[dom] > 0 else 0.0
@@ -402,6 +408,8 @@ class DeviceArm:
                 "rows_entering_each_live_layer": [int(x) for x in prof.live_rows[:-1][live_layers][:8]],
                 "live_layers": int(live_layers.size),
                 "live_edges_per_s": live_total * w.n * w.width / (ms_per_step * 1e-3),
+                # (tile, output) columns whose line bounds proved them all zero (no gather)
+                "pruned_columns": int(prof.pruned),
             },
             "roofline": {
                 "bound": "hbm",

@@ -184,6 +184,21 @@ int sdnn_result_launches(const sdnn_result *r, int64_t *n);
 int sdnn_net_set_compaction(sdnn_net *net, int pct);
 /* Row compactions the run performed (summed over waves / segments). */
 int sdnn_result_compactions(const sdnn_result *r, int64_t *n);
+/* Output pruning by line bounds.  Every stored line of activations (one
+ * neuron over a tile of rows) carries an upper bound of its largest |value|.
+ * For one output neuron of a tile, |chain| <= sum over its weight slots of
+ * |w| * (bound of the slot's input line); when that sum, with a margin far
+ * above the rounding of the chain, stays below -bias, the epilogue
+ * (engine.py:129-133: keep v = z + bias only when v > 0) stores nothing for
+ * any row of the tile, so the column gathers no line at all.  Data-dependent
+ * and exact: results are bit-identical with pruning off (on by default;
+ * `on` = 0 or SDNN_PRUNE=0 turns it off).  It uses no property of the weight
+ * values or of the layers beyond this run's own activations (PAPER.md
+ * avoid-list).  No reference counterpart: the reference's Gustavson product
+ * only ever touches stored entries. */
+int sdnn_net_set_pruning(sdnn_net *net, int on);
+/* (tile, output) columns the run pruned (summed over layers / waves). */
+int sdnn_result_pruned(const sdnn_result *r, int64_t *n);
 /* Final Y as canonical CSR (ascending columns, no zeros) widened to
  * float64: query nnz first, then fill caller buffers. */
 int sdnn_result_y_nnz(sdnn_result *r, int64_t *nnz);

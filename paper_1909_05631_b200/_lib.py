@@ -60,6 +60,8 @@ SIGNATURES = [
     ("sdnn_result_launches", cint, [vp, P(i64)]),
     ("sdnn_net_set_compaction", cint, [vp, cint]),
     ("sdnn_result_compactions", cint, [vp, P(i64)]),
+    ("sdnn_net_set_pruning", cint, [vp, cint]),
+    ("sdnn_result_pruned", cint, [vp, P(i64)]),
     ("sdnn_result_y_nnz", cint, [vp, P(i64)]),
     ("sdnn_result_y_csr", cint, [vp, vp, vp, vp]),
     ("sdnn_result_free", None, [vp]),

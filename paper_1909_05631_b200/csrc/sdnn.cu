@@ -153,6 +153,7 @@ struct sdnn_net {
     cudaEvent_t stage_ev[2] = {nullptr, nullptr};
     int layer_timing = 0;
     int compact_pct = 10;  // live-row compaction threshold (% of live tiles freed)
+    int prune = 1;         // output pruning by line bounds
     // weight-ingest scratch (CSR -> ELL on the device), grown on demand
     void* ing_pinned = nullptr;
     size_t ing_pinned_cap = 0;
@@ -183,6 +184,7 @@ struct sdnn_result {
     int64_t h2d_bytes = 0;  // host -> device bytes of the call's uploads (end-to-end calls)
     int64_t segments = 0;   // row segments of a streamed call
     int64_t compactions = 0;  // live-row compactions in the run
+    int64_t pruned = 0;       // (tile, output) columns pruned by their line bounds
     bool have_y = false;
     std::vector<int64_t> off, cols;
     std::vector<double> vals;
@@ -310,7 +312,11 @@ int64_t wave_rows(sdnn_net* net, int64_t n_rows, int64_t ld, int tr) {
     const int64_t per_tile = 2 * ld * (kLineBytes + 8);
     int64_t held = net->tcap_lines * (kLineBytes + 8) * 2;
     int64_t avail = (int64_t)free_b + held - (int64_t)(2ull << 30);
-    int64_t w = std::max<int64_t>(1, avail / per_tile) * tr;
+    // the layer kernels keep the wave's live-tile list and row prefix in
+    // dynamic shared memory ((2 * tiles + 1) * 4 bytes beside ~6 KB static):
+    // more tiles than fit there become more waves, not a capacity error
+    const int64_t smem_tiles = 24000;
+    int64_t w = std::min(std::max<int64_t>(1, avail / per_tile), smem_tiles) * tr;
     return std::min(w, std::max<int64_t>(n_rows, 1));
 }
 
@@ -626,7 +632,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
         if (int rc = grow(net->tile_count, c1, nl + 1, 4)) return rc;
         if (int rc = grow(net->live_rows, c2, nl + 1, 8)) return rc;
         if (int rc = grow(net->stamps, c3, nl + 1, 8)) return rc;
-        if (int rc = grow(net->work, c4, 2 * (nl + 1), 4)) return rc;  // layers, then compactions
+        if (int rc = grow(net->work, c4, 3 * (nl + 1), 4)) return rc;  // layers, compactions, pruned columns
         net->lcap = nl + 1;
     }
     int32_t* tile_count = net->tile_count;
@@ -645,7 +651,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     uint32_t* heap = net->heap;
     CK(cudaMemsetAsync(heap, 0, (nl + 1) * tiles1 * 4, net->stream));
     unsigned* work = net->work;
-    CK(cudaMemsetAsync(work, 0, 2 * std::max<int64_t>(nl, 1) * 4, net->stream));
+    CK(cudaMemsetAsync(work, 0, 3 * (nl + 1) * 4, net->stream));
     if (int rc = grow(net->alive_c, net->accap, tiles1 * AW, 4)) return rc;
     if (!net->n_compact) CK(cudaMalloc(&net->n_compact, 4));
     CK(cudaMemsetAsync(net->n_compact, 0, 4, net->stream));
@@ -680,6 +686,9 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     // pass over the live rows and a grid barrier (C1 as specified: 4 rows
     // left in 4 tiles, repacking them cost more than it saved)
     a.compact_min = std::max(1, env_int("SDNN_COMPACT_MIN", 16));
+    // output pruning by line bounds (sdnn_net_set_pruning; SDNN_PRUNE=0 turns it off)
+    a.prune = epilogue ? env_int("SDNN_PRUNE", net->prune) : 0;  // raw Z (engine.spmm) keeps every entry
+    a.pruned = work + 2 * (nl + 1);
     a.jb = env_int("SDNN_JB", net->jb);
     // dense inputs (>= 60 % of sectors kept): 64-output items -- measured on
     // the K2 companion's dense layers, 36.7 -> 29.9 ms at JB 256 -> 64; C4's
@@ -777,6 +786,8 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     std::vector<uint32_t> alive_last(tiles1 * AW);
     std::vector<int32_t> rowid(n_tiles * TR);
     int n_compact = 0;
+    std::vector<unsigned> pruned(nl + 1);
+    CK(cudaMemcpyAsync(pruned.data(), a.pruned, (nl + 1) * 4, cudaMemcpyDeviceToHost, net->stream));
     CK(cudaMemcpyAsync(&n_compact, net->n_compact, 4, cudaMemcpyDeviceToHost, net->stream));
     CK(cudaMemcpyAsync(lr.data(), live, (nl + 1) * 8, cudaMemcpyDeviceToHost, net->stream));
     CK(cudaMemcpyAsync(st.data(), stamps, (nl + 1) * 8, cudaMemcpyDeviceToHost, net->stream));
@@ -787,6 +798,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     // and the final slab in the other parity
     if (n_compact & 1) net->rowid = net->rowid_alt;
     res->compactions += n_compact;
+    for (unsigned c : pruned) res->pruned += c;
     if (n_tiles) CK(cudaMemcpy(rowid.data(), net->rowid, n_tiles * TR * 4, cudaMemcpyDeviceToHost));
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, net->ev0, net->ev1));
@@ -1283,6 +1295,7 @@ void merge_part(sdnn_result* res, const sdnn_result& part, int64_t r0, int want_
     res->dev_ms += part.dev_ms;
     res->launches += part.launches;
     res->compactions += part.compactions;
+    res->pruned += part.pruned;
     for (int k = 0; k < 3; ++k) res->stage_ms[k] += part.stage_ms[k];
     for (size_t l = 0; l < part.layer_ms.size() && l < res->layer_ms.size(); ++l) res->layer_ms[l] += part.layer_ms[l];
     if (want_y) {
@@ -1887,6 +1900,18 @@ int sdnn_result_compactions(const sdnn_result* r, int64_t* n) {
     return SDNN_OK;
 }
 
+int sdnn_net_set_pruning(sdnn_net* net, int on) {
+    if (!net) return fail(SDNN_ERR_PARAMETER, "null argument");
+    net->prune = on ? 1 : 0;
+    return SDNN_OK;
+}
+
+int sdnn_result_pruned(const sdnn_result* r, int64_t* n) {
+    if (!r || !n) return fail(SDNN_ERR_PARAMETER, "null argument");
+    *n = r->pruned;
+    return SDNN_OK;
+}
+
 int sdnn_result_stage_ms(const sdnn_result* r, double* ms) {
     if (!r || !ms) return fail(SDNN_ERR_PARAMETER, "null argument");
     for (int i = 0; i < 3; ++i) ms[i] = r->stage_ms[i];
@@ -2055,6 +2080,7 @@ int sdnn_group_infer(sdnn_group* g, int64_t n_rows, const int64_t* y_off, const 
             for (int k = 0; k < 3; ++k) res->stage_ms[k] = std::max(res->stage_ms[k], p.stage_ms[k]);
             res->launches += p.launches;
             res->compactions += p.compactions;
+            res->pruned += p.pruned;
             res->h2d_bytes += p.h2d_bytes;
             res->segments += p.segments;
             if (want_y) {

@@ -25,8 +25,9 @@
 // lanes x one 32-byte sector: lane l owns rows l*RPL .. l*RPL+RPL-1
 // (RPL = 32 B / sizeof(T)), read with one 256-bit load.  Lines are stored
 // sector-compressed: only sectors holding a nonzero are kept, packed in lane
-// order, in the tile's sector heap; meta[(tile, neuron)] = {lane mask of the
-// kept sectors, heap index of the first}.  A warp computes one output column
+// order, at the front of the line's own 1 KB slot; meta[(tile, neuron)] =
+// {lane mask of the kept sectors, upper bound of the line's largest |value|
+// as float bits}.  A warp computes one output column
 // of a tile: per weight slot it gathers one line (each live lane its sector,
 // dead lanes read a shared zero sector), so one weight slot serves TR rows.
 // Slots whose whole line is zero are dropped from the warp's slot list
@@ -105,6 +106,37 @@ __device__ __forceinline__ T bias_relu_clamp_stored(T z, T bias, T ymax) {
 #endif
 __device__ __forceinline__ unsigned sector_pos(unsigned mask, int lane) {
     return SDNN_PACKED ? (unsigned)__popc(mask & ((1u << lane) - 1u)) : (unsigned)lane;
+}
+
+// Line bound (meta.y of a value line): an upper bound of the largest |value|
+// the line holds, as float bits (0 for an empty line).  Nonnegative floats
+// order like their bit patterns, so a line's bound is one integer max over
+// the lanes (REDUX); a double is rounded up to float first.  A NaN value
+// gives a NaN bound (its bits exceed +inf's), which never prunes.
+// Every value line sits in its own 1 KB slot (sector k*32 of the tile), so
+// the meta needs no heap index; bit-line metas keep {mask, heap index}.
+__device__ __forceinline__ unsigned bound_bits(float v) { return __float_as_uint(fabsf(v)); }
+__device__ __forceinline__ unsigned bound_bits(double v) { return __float_as_uint(__double2float_ru(fabs(v))); }
+// |w| rounded up to float, and an upper bound of 2^20 / -bias (bias < 0): the
+// approximate reciprocal is within 2^-23 of the true one, the factor
+// 2^20 + 4 and the upward rounding keep the product above it.
+__device__ __forceinline__ float bound_up(float w) { return fabsf(w); }
+__device__ __forceinline__ float bound_up(double w) { return __double2float_ru(fabs(w)); }
+__device__ __forceinline__ float bias_toward_zero(float b) { return b; }
+__device__ __forceinline__ float bias_toward_zero(double b) { return __double2float_rz(b); }
+template <typename T>
+__device__ __forceinline__ float prune_scale(T bias) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(-bias_toward_zero(bias)));
+    return __fmul_ru(r, 1048580.f);
+}
+template <typename T, int R>
+__device__ __forceinline__ unsigned lane_bound(const T (&v)[R]) {
+    unsigned b = 0u;
+#pragma unroll
+    for (int c = 0; c + 1 < R; c += 2) b = __vimax3_u32(b, bound_bits(v[c]), bound_bits(v[c + 1]));
+    if (R & 1) b = max(b, bound_bits(v[R - 1]));
+    return b;
 }
 
 // Tile geometry.
@@ -234,7 +266,8 @@ struct NetArgs {
     int epilogue;         // 1: bias/ReLU/clamp; 0: raw Z (engine.spmm)
     int n_tiles;
     T* slab[2];           // [n_tiles][ld * 32 sectors of 32 B] sector heaps
-    uint2* meta[2];       // [n_tiles][ld] {kept-sector lane mask, heap index}
+    uint2* meta[2];       // [n_tiles][ld] value lines: {kept-sector lane mask, line bound (float bits)};
+                          // bit-lines: {mask, heap index}
     uint32_t* heap;       // [L + 1][n_tiles] sectors used in each layer's heap
     const T* zero;        // one all-zero 32-byte sector
     uint32_t* alive;      // [L + 1][n_tiles][alive_words] live-row bitmap + flag
@@ -258,6 +291,11 @@ struct NetArgs {
     // narrower item window keeps the tile being gathered inside L2)
     int jb_dense;
     int dense_pct;
+    // output pruning by bound: a column of a tile whose 32 input lines cannot
+    // lift any row above -bias (sum of |w| * line bound, with a rounding
+    // margin) is all zero after the epilogue and gathers nothing
+    int prune;
+    unsigned* pruned;     // [L] (tile, output) columns pruned per layer, or null
 };
 constexpr int kDensitySample = 256;  // input lines sampled per layer (the same ones in every CTA)
 
@@ -433,11 +471,15 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_kernel(const int64_t*
                 bool any = false;
 #pragma unroll
                 for (int c = 0; c < rows_per_lane<T>(); ++c) any |= sv[c] != T(0);
+                unsigned vb = 0u;
+#pragma unroll
+                for (int c = 0; c < rows_per_lane<T>(); ++c) vb = max(vb, bound_bits(sv[c]));
                 const unsigned m = __ballot_sync(0xffffffffu, any);
+                vb = __reduce_max_sync(0xffffffffu, vb);
                 // the line's kept sectors go into its own 1 KB slot
                 const unsigned base = (unsigned)(k0 + k) * 32u;
                 if (any) st32_bits(s0 + (size_t)(base + sector_pos(m, lane)) * 32, a, b);
-                if (lane == 0) gm[k0 + k] = make_uint2(m, base);
+                if (lane == 0) gm[k0 + k] = make_uint2(m, vb);
                 src[0] = z4;  // re-zero for the next chunk
                 src[1] = z4;
             }
@@ -680,15 +722,32 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
         }
         const uint2 m1 = (b + 1 < total && k1 >= 0) ? imeta[k1] : make_uint2(0u, 0u);
 
-        const unsigned live = __ballot_sync(0xffffffffu, m0.x != 0u);
+        // output pruning: |chain| <= sum of |w| * line bound.  Each lane's
+        // term, divided by -bias and scaled by 2^20, is rounded UP to an
+        // integer (every float step rounds up; NaN or huge terms clamp to
+        // 2^26, which alone exceeds the threshold), the warp adds them with
+        // one REDUX, and a sum at most 2^20 - 2^10 (the 2^-10 margin is far
+        // above the rounding of a 32-step chain) proves that every row of
+        // the column ends <= 0: the epilogue stores nothing, so the column
+        // gathers no line
+        unsigned mx = m0.x;
+        if (!BIN && a.prune && L.wp == 32 && L.bias < T(0)) {
+            const float c = __fmul_ru(bound_up(w0), __uint_as_float(m0.y));
+            const float q = fminf(__fmul_ru(mx ? c : 0.f, prune_scale(L.bias)), 67108864.f);
+            if (__reduce_add_sync(0xffffffffu, __float2uint_ru(q)) <= 1048576u - 1024u) {
+                mx = 0u;
+                alive_bits += 0x10000u;  // pruned columns are counted above the row bits
+            }
+        }
+        const unsigned live = __ballot_sync(0xffffffffu, mx != 0u);
         const int n = __popc(live);
         const int npad = (n + GB - 1) / GB * GB;
         {
             SlotEntry<T> e;
             int at;
-            if (m0.x) {
-                e.base = m0.y;
-                e.mask = m0.x;
+            if (mx) {
+                e.base = BIN ? m0.y : (unsigned)k0 * 32u;  // value lines: the line's own slot
+                e.mask = mx;
                 e.w = w0;
                 at = __popc(live & below);
             } else {  // padding: no lane gathers it
@@ -801,7 +860,8 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
             const unsigned om = __ballot_sync(0xffffffffu, bits != 0u);
             const unsigned hb = (unsigned)cj * 32u;
             if (bits) st32(out + (size_t)(hb + sector_pos(om, lane)) * 32, v);
-            if (lane == 0) ometa[cj] = make_uint2(om, hb);
+            const unsigned ob = om ? __reduce_max_sync(0xffffffffu, lane_bound(v)) : 0u;
+            if (lane == 0) ometa[cj] = make_uint2(om, ob);
             alive_bits |= bits;
             cj += kWarps;
         }
@@ -811,6 +871,8 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
         k1 = k2;
         w1 = w2;
     }
+    if (!BIN && (alive_bits >> 16) && a.pruned && lane == 0) atomicAdd(&a.pruned[l], alive_bits >> 16);
+    alive_bits &= 0xFFFFu;
     // live rows of this warp's columns -> the tile's row bitmap
     if (__any_sync(0xffffffffu, alive_bits != 0u))
         publish_alive<T>(a.alive + ((size_t)(l + 1) * a.n_tiles + t) * AW, alive_bits, &a.tile_count[l + 1]);
@@ -969,7 +1031,8 @@ __device__ __forceinline__ void bin_item2(const NetArgs<float>& a, const LayerDe
                 const unsigned hb = (unsigned)cj * 32u;
                 char* out = reinterpret_cast<char*>(a.slab[1]) + lines * kLineBytes;
                 if (bits) st32(out + (size_t)(hb + sector_pos(om, lane)) * 32, v);
-                if (lane == 0) a.meta[1][lines + cj] = make_uint2(om, hb);
+                const unsigned ob = om ? __reduce_max_sync(0xffffffffu, lane_bound(v)) : 0u;
+                if (lane == 0) a.meta[1][lines + cj] = make_uint2(om, ob);
                 alive_bits |= bits;
             };
             finish(accA, linesA, aliveA);
@@ -1290,8 +1353,14 @@ __device__ __forceinline__ void bin_quad_item(const NetArgs<T>& a, const LayerDe
             }
             // the tile's sector mask: lane sub contributes bits SPL*sub .. SPL*sub+SPL-1
             unsigned m = piece << (SPL * sub);
+            unsigned ob = 0u;  // the tile's line bound: max over its LPT lanes
 #pragma unroll
-            for (int x = 1; x < LPT; x <<= 1) m |= __shfl_xor_sync(0xffffffffu, m, x);
+            for (int g = 0; g < SPL; ++g) ob = max(ob, lane_bound(v[g]));
+#pragma unroll
+            for (int x = 1; x < LPT; x <<= 1) {
+                m |= __shfl_xor_sync(0xffffffffu, m, x);
+                ob = max(ob, __shfl_xor_sync(0xffffffffu, ob, x));
+            }
             const unsigned hb = (unsigned)cj * 32u;
             if (tile_ok) {
 #pragma unroll
@@ -1299,7 +1368,7 @@ __device__ __forceinline__ void bin_quad_item(const NetArgs<T>& a, const LayerDe
                     const unsigned lp = (unsigned)(sub * SPL + g);
                     if ((piece >> g) & 1u) st32(out + (size_t)(hb + __popc(m & ((1u << lp) - 1u))) * 32, v[g]);
                 }
-                if (sub == 0) ometa[cj] = make_uint2(m, hb);
+                if (sub == 0) ometa[cj] = make_uint2(m, ob);
             }
             alive32 |= bits32;
             cj += kWarps;
@@ -1479,14 +1548,16 @@ __device__ __forceinline__ void compact_pass(const NetArgs<T>& a, int l, bool od
                     const size_t tl = (size_t)ot * a.ld;
                     const uint2 m = imeta[tl + k];
                     if ((m.x >> sec) & 1u)
-                        v[c] = in[(tl * 32 + m.y + (unsigned)__popc(m.x & ((1u << sec) - 1u))) * RPL + orow % RPL];
+                        v[c] = in[(tl * 32 + (unsigned)k * 32u + (unsigned)__popc(m.x & ((1u << sec) - 1u))) * RPL +
+                                  orow % RPL];
                 }
                 bits |= (v[c] != T(0)) ? (1u << c) : 0u;
             }
             const unsigned om = __ballot_sync(0xffffffffu, bits != 0u);
             const unsigned hb = (unsigned)k * 32u;
             if (bits) st32(reinterpret_cast<char*>(out + (tl_out * 32 + hb + sector_pos(om, lane)) * RPL), v);
-            if (lane == 0) ometa[tl_out + k] = make_uint2(om, hb);
+            const unsigned ob = om ? __reduce_max_sync(0xffffffffu, lane_bound(v)) : 0u;
+            if (lane == 0) ometa[tl_out + k] = make_uint2(om, ob);
         }
         __syncthreads();  // sh.src / sh.item are rewritten by the next item
     }
@@ -1567,7 +1638,7 @@ __global__ void extract_kernel(const T* __restrict__ slab, const uint2* __restri
         for (int k = 0; k < n_cols; ++k) {
             const uint2 mk = m[k];
             if (!(mk.x & lbit)) continue;
-            const T* sec = s + (size_t)(mk.y + sector_pos(mk.x, lane)) * RPL;
+            const T* sec = s + (size_t)((unsigned)k * 32u + sector_pos(mk.x, lane)) * RPL;
 #pragma unroll
             for (int q = 0; q < RPL; ++q) {
                 const T v = sec[q];
@@ -1634,7 +1705,7 @@ __global__ void extract_rows_kernel(const T* __restrict__ slab, const uint2* __r
         for (int k = 0; k < n_cols; ++k) {
             const uint2 mk = m[k];
             if (!(mk.x & lbit)) continue;
-            const T* sec = s + (size_t)(mk.y + sector_pos(mk.x, lane)) * RPL;
+            const T* sec = s + (size_t)((unsigned)k * 32u + sector_pos(mk.x, lane)) * RPL;
 #pragma unroll
             for (int q = 0; q < RPL; ++q) {
                 const T v = sec[q];

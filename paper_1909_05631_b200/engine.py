@@ -155,6 +155,7 @@ class RunResult:
     h2d_bytes: int = 0          # end-to-end calls: host -> device bytes copied
     segments: int = 0           # end-to-end calls: row segments streamed
     compactions: int = 0        # live-row repacks between layers
+    pruned: int = 0             # (tile, output) columns pruned by their line bounds
 
 
 class DeviceBatch:
@@ -303,6 +304,12 @@ class DeviceNetwork:
         """Repack live rows densely before a layer once that frees >= pct % of
         the live tiles (<= 0: never).  Bit-identical results either way."""
         _lib.check(_lib.lib().sdnn_net_set_compaction(self.handle, int(pct)))
+
+    def set_pruning(self, on: bool) -> None:
+        """Output pruning by line bounds (include/sdnn.h): columns whose input
+        lines cannot lift any row above -bias gather nothing.  Bit-identical
+        results either way."""
+        _lib.check(_lib.lib().sdnn_net_set_pruning(self.handle, 1 if on else 0))
 
     def weight_bytes(self) -> int:
         b = ctypes.c_int64()
@@ -502,6 +509,8 @@ def _collect(h, n_rows: int, want_y: bool) -> RunResult:
     _lib.check(L.sdnn_result_stage_ms(h, _lib.ptr(stage_ms)))
     comp = ctypes.c_int64()
     _lib.check(L.sdnn_result_compactions(h, ctypes.byref(comp)))
+    pruned = ctypes.c_int64()
+    _lib.check(L.sdnn_result_pruned(h, ctypes.byref(pruned)))
     y = None
     if want_y:
         nnz = ctypes.c_int64()
@@ -512,7 +521,7 @@ def _collect(h, n_rows: int, want_y: bool) -> RunResult:
         _lib.check(L.sdnn_result_y_csr(h, _lib.ptr(off), _lib.ptr(cols), _lib.ptr(vals)))
         y = (off, cols[:nnz.value], vals[:nnz.value])
     return RunResult(cats, live, L.sdnn_result_device_ms(h), L.sdnn_result_wall_ms(h),
-                     launches.value, y, layer_ms, stage_ms, compactions=comp.value)
+                     launches.value, y, layer_ms, stage_ms, compactions=comp.value, pruned=pruned.value)
 
 
 # ------------------------------------------------------- network residency

@@ -1,0 +1,149 @@
+"""Output pruning by line bounds (include/sdnn.h: sdnn_net_set_pruning).
+
+A (tile, output) column whose input lines cannot lift any row above -bias
+gathers nothing.  The bound is an upper bound of the chain the reference
+computes (engine.py:64-137), so the result must be bit-identical with
+pruning on and off and equal to the oracle's, on the BASELINE dynamics
+(rows die at layer 2-3: on the flagship almost every column of the dying
+layer is pruned),
+on live rows (nothing may be pruned away), on mixed-sign general instances
+and at the rounding boundary of `sum == -bias`.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1909_05631_b200 import engine as E  # noqa: E402
+from paper_1909_05631_b200 import workloads as W  # noqa: E402
+from paper_1909_05631_b200.model import SparseMatrix  # noqa: E402
+
+
+def sm(c: O.CSR) -> SparseMatrix:
+    return SparseMatrix(c.n_rows, c.n_cols, c.off, c.cols, c.vals, check=False)
+
+
+def both(net, batch, ymax):
+    """(pruning on, pruning off) runs of one staged batch, asserted identical."""
+    net.set_pruning(True)
+    on = net.run(batch, ymax, want_y=True)
+    net.set_pruning(False)
+    off = net.run(batch, ymax, want_y=True)
+    net.set_pruning(True)
+    assert off.pruned == 0
+    assert all(np.array_equal(a, b) for a, b in zip(on.y, off.y))
+    assert np.array_equal(on.categories, off.categories)
+    assert np.array_equal(on.live_rows, off.live_rows)
+    return on, off
+
+
+@pytest.mark.parametrize("dtype,prec", [("f32", 32), ("f64", 64)])
+@pytest.mark.parametrize("name,rows,layers", [("C1", 3000, 12), ("C2", 1500, 8), ("C4", 700, 6)])
+def test_dying_configs_are_pruned_and_bit_identical(name, rows, layers, dtype, prec):
+    """BASELINE dynamics (w = 0.0625): layer 2's inputs are few and small,
+    its columns are pruned, and the result is the oracle's."""
+    w = W.CONFIGS[name].with_(batch=rows, layers=layers)
+    off, cols, vals = W.images(w)
+    y0 = O.CSR(rows, w.n, off, cols, vals)
+    net = E.DeviceNetwork(w.n, 0, dtype)
+    net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias)
+    on, _ = both(net, net.upload_csr(rows, off, cols, vals), w.ymax)
+    lw = [O.CSR(w.n, w.n, *W.layer_csr(w, l)) for l in range(w.layers)]
+    want = O.infer(lw, [w.bias] * w.layers, y0, w.ymax, precision=prec, threads=8)
+    assert O.CSR(rows, w.n, *on.y).identical(want)
+    assert np.array_equal(on.categories, O.categorize(want))
+    # layer 2 runs in the persistent kernel over every (tile, output).  C4's
+    # layer-1 outputs are 5 % dense and at most ~0.3, so 32 * 0.0625 * (line
+    # bound) stays below 0.45 for nearly every column; C1 / C2 (47 % / 26 %
+    # dense, bias -0.30 / -0.35) are beyond a line-granular bound and simply
+    # gather as before
+    if name == "C4":
+        tiles = -(-int(on.live_rows[1]) // (256 if dtype == "f32" else 128))
+        assert on.pruned >= tiles * w.n * 8 // 10, (on.pruned, tiles * w.n)
+    net.close()
+
+
+@pytest.mark.parametrize("dtype,prec", [("f32", 32), ("f64", 64)])
+@pytest.mark.parametrize("bits", ["1", "0"])
+def test_live_rows_survive_pruning(monkeypatch, dtype, prec, bits):
+    """Rows that stay alive (w = 0.125) and rows that die gradually share
+    tiles: pruning may only drop columns that end at zero for every row."""
+    monkeypatch.setenv("SDNN_BIN", bits)
+    side = 32
+    w = W.Workload("t", 1024, 10, 2000, side, 20, 0.35, -0.45, value=0.125)
+    off, cols, vals = W.images(w)
+    y0 = O.CSR(w.batch, w.n, off, cols, vals)
+    lw = [O.CSR(w.n, w.n, *W.layer_csr(w, l)) for l in range(w.layers)]
+    want = O.infer(lw, [w.bias] * w.layers, y0, w.ymax, precision=prec, threads=8)
+    assert 0 < O.categorize(want).size < w.batch
+    net = E.DeviceNetwork(w.n, 0, dtype)
+    net.add_permunion_layers(w.weight_seed, 0, w.layers, w.width, w.value, w.bias)
+    on, _ = both(net, net.upload_csr(w.batch, off, cols, vals), w.ymax)
+    assert O.CSR(w.batch, w.n, *on.y).identical(want)
+    net.close()
+
+
+def test_mixed_sign_general_instances():
+    """Mixed-sign weights, variable degree (ELL padded to 32 slots), biases of
+    either sign, real-valued inputs: on == off == oracle, float64."""
+    rng = np.random.default_rng(5631)
+    pruned = 0
+    for i in range(60):
+        n = int(rng.integers(8, 97))
+        layers, bias = [], []
+        for _ in range(int(rng.integers(1, 7))):
+            dens = rng.uniform(0.02, 0.3)
+            m = np.where(rng.random((n, n)) < dens, rng.uniform(-1, 1, (n, n)), 0.0)
+            layers.append(O.CSR.from_dense(m))
+            bias.append(float(rng.uniform(-0.8, 0.2)))
+        rows = int(rng.integers(1, 300))
+        y = (rng.random((rows, n)) < rng.uniform(0.05, 0.6)).astype(np.float64)
+        y *= rng.uniform(0.05, 2.0, y.shape)
+        y0 = O.CSR.from_dense(y)
+        net = E.DeviceNetwork(n, 0, "f64")
+        for m, b in zip(layers, bias):
+            net.add_layer_csr(sm(m), b)
+        on, _ = both(net, net.upload_csr(rows, y0.off, y0.cols, y0.vals), 32.0)
+        want = O.infer(layers, bias, y0, precision=64)
+        assert O.CSR(rows, n, *on.y).identical(want), i
+        pruned += on.pruned
+        net.close()
+    assert pruned > 0  # the bound fires on some of them
+
+
+@pytest.mark.parametrize("dtype,prec", [("f32", 32), ("f64", 64)])
+def test_rounding_boundary(dtype, prec):
+    """Every output sums 32 inputs of value y with weight 1/16: z = 2y.  With
+    bias = -(2y) the result is exactly zero (dropped); one ulp less negative
+    and every entry survives with a tiny value.  The bound must not prune
+    the second case (its margin only ever errs towards gathering)."""
+    n, rows = 64, 300
+    dense = np.zeros((n, n))
+    for j in range(n):
+        for s in range(32):
+            dense[(j + s) % n, j] = 0.0625
+    wm = O.CSR.from_dense(dense)
+    yv = 1.7
+    y = np.full((rows, n), yv)
+    y0 = O.CSR.from_dense(y)
+    ft = np.float32 if prec == 32 else np.float64
+    z = ft(0)
+    for _ in range(32):  # the chain's own rounding
+        z = ft(z + ft(yv) * ft(0.0625))  # the product is exact (power-of-two weight)
+    exact = -float(z)
+    for bias, survive in ((exact, False), (float(np.nextafter(ft(exact), ft(0))), True),
+                          (exact * 1.0005, False), (exact * 0.9995, True)):
+        net = E.DeviceNetwork(n, 0, dtype)
+        net.add_layer_csr(sm(wm), bias)
+        on, _ = both(net, net.upload_csr(rows, y0.off, y0.cols, y0.vals), 32.0)
+        want = O.infer([wm], [bias], y0, precision=prec)
+        assert O.CSR(rows, n, *on.y).identical(want), bias
+        assert (on.categories.size == rows) == survive, bias
+        net.close()
