@@ -675,6 +675,7 @@ def companions(args):
             "live_rows_last_layer": int(p.live_rows[-2]),
             "categories": int(r.categories.size),
             "row_compactions": int(r.compactions),
+            "pruned_columns": int(r.pruned),
             "ms_per_step_without_compaction": r0.device_ms,
             "steady_layer_ms": float(p.layer_ms[mid]),
             "steady_layer_gbs": gbs,

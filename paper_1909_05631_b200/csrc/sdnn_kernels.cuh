@@ -735,8 +735,17 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
             const float c = __fmul_ru(bound_up(w0), __uint_as_float(m0.y));
             const float q = fminf(__fmul_ru(mx ? c : 0.f, prune_scale(L.bias)), 67108864.f);
             if (__reduce_add_sync(0xffffffffu, __float2uint_ru(q)) <= 1048576u - 1024u) {
-                mx = 0u;
+                // the column (one batch) is complete and empty: its chains are
+                // still zero, nothing to list, gather or store but the meta
                 alive_bits += 0x10000u;  // pruned columns are counted above the row bits
+                if (lane == 0) ometa[cj] = make_uint2(0u, 0u);
+                cj += kWarps;
+                k0 = k1;
+                w0 = w1;
+                m0 = m1;
+                k1 = k2;
+                w1 = w2;
+                continue;
             }
         }
         const unsigned live = __ballot_sync(0xffffffffu, mx != 0u);
