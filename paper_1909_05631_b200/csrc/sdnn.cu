@@ -757,8 +757,12 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     if (a.bin_in && quad) {  // layer 1 over quad / oct bit-lines: its own launch
         const void* qfn = (const void*)bin_quad_kernel<T>;
         int qocc = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&qocc, qfn, kThreads, 0));
-        bin_quad_kernel<T><<<net->sm_count * std::max(qocc, 1), kThreads, 0, net->stream>>>(a);
+        // row prefilter (SDNN_PREFILTER=0 turns it off): per-warp staging tile in dynamic shared memory
+        a.prefilter = a.prune ? env_int("SDNN_PREFILTER", 1) : 0;
+        const size_t qsmem = a.prefilter ? (size_t)kWarps * quad_warp_smem<T>() : 0;
+        CK(cudaFuncSetAttribute(qfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsmem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&qocc, qfn, kThreads, qsmem));
+        bin_quad_kernel<T><<<net->sm_count * std::max(qocc, 1), kThreads, qsmem, net->stream>>>(a);
         CK(cudaGetLastError());
         res->launches += 1;
         a.first_l = 1;

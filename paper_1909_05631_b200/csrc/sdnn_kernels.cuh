@@ -296,6 +296,8 @@ struct NetArgs {
     // margin) is all zero after the epilogue and gathers nothing
     int prune;
     unsigned* pruned;     // [L] (tile, output) columns pruned per layer, or null
+    int prefilter;        // layer 1 over quad/oct bit-lines: exact chains only for rows whose set-input
+                          // count could reach -bias (bin_quad_item1)
 };
 constexpr int kDensitySample = 256;  // input lines sampled per layer (the same ones in every CTA)
 
@@ -1397,14 +1399,309 @@ __device__ __forceinline__ void bin_quad_item(const NetArgs<T>& a, const LayerDe
         atomicAdd(&a.tile_count[1], 1);
 }
 
+// ---- layer 1 with a row prefilter (one batch per column, real epilogue, bias < 0)
+// A row's chain over bit-lines is at most (number of its set inputs) * wmax,
+// wmax the column's largest |weight|.  The set inputs of all 32 rows of a
+// lane's word are counted at once with a bit-sliced carry-save adder (two
+// 3-input logic ops per full adder, ~2.4 per slot instead of 32 predicated
+// adds), the counts are compared bit-sliced with the smallest count Kt that
+// could reach -bias, and only the rows that pass ("maybe" rows; 5 % on the
+// flagship's Y0) get their exact chain: they are listed in shared memory,
+// each lane takes one or two of them, walks the column's slot list (one word
+// load per slot, the same ascending order and the same additions as the
+// dense walk, so the same bits), applies the epilogue and drops the value
+// into the warp's staging tile, from which every lane reads back its own 32
+// rows for the usual sector stores.  Columns with more than 64 maybe rows take
+// the dense walk.  Exact: the count bound only ever errs towards "maybe"
+// (weights rounded up, -bias scaled by 1 - 2^-10 and rounded down).
+__device__ __forceinline__ void csa(unsigned& h, unsigned& l, unsigned x, unsigned y, unsigned z) {
+    const unsigned u = x ^ y;
+    h = (x & y) | (u & z);
+    l = u ^ z;
+}
+constexpr int kMaybeRows = 64;  // listed rows per column (two per lane)
+template <typename T>
+__host__ __device__ constexpr int quad_warp_smem() {  // staging tile + weights + row list, per warp
+    return 1024 * (int)sizeof(T) + 32 * (int)sizeof(T) + kMaybeRows * 2;
+}
+// staging tile: row c of word (lane) wi, 16-byte chunks XOR-swizzled by the
+// word so that the owners' 128-bit read-back is conflict-free
+template <typename T>
+__device__ __forceinline__ int stage_pos(int wi, int c) {
+    constexpr int EPC = 16 / (int)sizeof(T);  // elements per 16-byte chunk
+    return wi * 32 + (((c / EPC) ^ (wi & 7)) * EPC) + c % EPC;
+}
+
+// One column's final values (each lane the 32 rows of its word) -> its
+// tile's kept sectors, sector mask and line bound; returns the lane's live rows.
+template <typename T>
+__device__ __forceinline__ unsigned quad_store(const T (&v)[32 / rows_per_lane<T>()][rows_per_lane<T>()], char* out,
+                                               uint2* ometa, int cj, int sub, bool tile_ok) {
+    constexpr int RPL = rows_per_lane<T>(), SPL = 32 / RPL, LPT = 32 / quad_tiles<T>();
+    unsigned piece = 0u, bits32 = 0u, ob = 0u;
+#pragma unroll
+    for (int g = 0; g < SPL; ++g) {
+        unsigned bits = 0u;
+#pragma unroll
+        for (int c = 0; c < RPL; ++c) bits |= (v[g][c] != T(0)) ? (1u << c) : 0u;
+        piece |= bits ? (1u << g) : 0u;
+        bits32 |= bits << (g * RPL);
+        ob = max(ob, lane_bound(v[g]));
+    }
+    unsigned m = piece << (SPL * sub);
+#pragma unroll
+    for (int x = 1; x < LPT; x <<= 1) {
+        m |= __shfl_xor_sync(0xffffffffu, m, x);
+        ob = max(ob, __shfl_xor_sync(0xffffffffu, ob, x));
+    }
+    const unsigned hb = (unsigned)cj * 32u;
+    if (tile_ok) {
+#pragma unroll
+        for (int g = 0; g < SPL; ++g) {
+            const unsigned lp = (unsigned)(sub * SPL + g);
+            if ((piece >> g) & 1u) st32(out + (size_t)(hb + __popc(m & ((1u << lp) - 1u))) * 32, v[g]);
+        }
+        if (sub == 0) ometa[cj] = make_uint2(m, ob);
+    }
+    return bits32;
+}
+
+template <typename T, int GB>
+__device__ __forceinline__ void bin_quad_item1(const NetArgs<T>& a, const LayerDesc<T>& L, int q, int j0, int j1,
+                                               uint2* wlist, unsigned char* wsmem) {
+    using A = Arith<T>;
+    constexpr int AW = alive_words<T>(), RPL = rows_per_lane<T>();
+    constexpr int TPQ = quad_tiles<T>(), LPT = 32 / TPQ, SPL = 32 / RPL;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int T_ = lane / LPT, sub = lane % LPT;
+    const unsigned below = (1u << lane) - 1u;
+    const int t0 = q * TPQ, ntq = min(TPQ, a.n_tiles - t0);
+    const int t = t0 + min(T_, ntq - 1);
+    const bool tile_ok = T_ < ntq;
+    const unsigned* inq0 =
+        reinterpret_cast<const unsigned*>(reinterpret_cast<const char*>(a.slab[0]) + (size_t)q * a.ld * kQuadLine);
+    const unsigned* inq = inq0 + lane;
+    asm("mov.b64 %0, %0;" : "+l"(inq));
+    T* stage = reinterpret_cast<T*>(wsmem);
+    T* wsm = stage + 1024;
+    unsigned short* rows = reinterpret_cast<unsigned short*>(wsm + 32);
+    const size_t tile_lines = (size_t)t * a.ld;
+    char* out = reinterpret_cast<char*>(a.slab[1]) + tile_lines * kLineBytes;
+    uint2* ometa = a.meta[1] + tile_lines;
+    const uint2* m0p = a.meta[0] + (size_t)q * a.ld;
+    const int jw = j0 + warp;
+    if (jw >= j1) return;
+    const int n_cols = (j1 - jw + kWarps - 1) / kWarps;
+    size_t po = (size_t)jw * 32 + lane;
+    const size_t col_step = (size_t)kWarps * 32;
+    auto quad_live = [&](int k) -> bool { return k >= 0 && m0p[k].x != 0u; };
+    const uint64_t wpol = policy_evict_last();
+    int k0 = ld_w(L.idx + po, wpol);
+    T w0 = ld_w(L.val + po, wpol);
+    po += col_step;
+    int k1 = -1, k2 = -1;
+    T w1 = T(0), w2 = T(0);
+    if (n_cols > 1) {
+        k1 = ld_w(L.idx + po, wpol);
+        w1 = ld_w(L.val + po, wpol);
+        po += col_step;
+    }
+    bool l0 = quad_live(k0);
+    unsigned alive32 = 0u;
+    int cj = jw;
+    // -bias * (1 - 2^-10), rounded down: a row reaches it only with count >= Kt
+    const float reach = __fmul_rd(-bias_toward_zero(L.bias), 0.9990234375f);
+    for (int b = 0; b < n_cols; ++b) {
+        if (b + 2 < n_cols) {
+            k2 = ld_w(L.idx + po, wpol);
+            w2 = ld_w(L.val + po, wpol);
+            po += col_step;
+        }
+        const bool l1 = (b + 1 < n_cols) ? quad_live(k1) : false;
+        const unsigned live = __ballot_sync(0xffffffffu, l0);
+        const int n = __popc(live);
+        const int npad = (n + GB - 1) / GB * GB;
+        {
+            uint2 e;
+            int at;
+            if (l0) {
+                e = make_uint2((unsigned)k0 * (kQuadLine / 4), sizeof(T) == 4 ? __float_as_uint((float)w0) : 0u);
+                at = __popc(live & below);
+            } else {  // padding: word 0 of line 0, weight 0 (adds +0)
+                e = make_uint2(0u, 0u);
+                at = n + __popc(~live & below);
+            }
+            if (at < npad) {
+                wlist[at] = e;
+                wsm[at] = l0 ? w0 : T(0);
+            }
+        }
+        const unsigned wmb = __reduce_max_sync(0xffffffffu, l0 ? __float_as_uint(bound_up(w0)) : 0u);
+        __syncwarp();
+        // ---- count the set inputs of every row (bit-sliced, 8 slots a round)
+        unsigned ones = 0u, twos = 0u, fours = 0u, eights = 0u, sixteens = 0u, thirtytwo = 0u;
+        for (int i0 = 0; i0 < n; i0 += 8) {
+            unsigned d[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const unsigned off = wlist[i0 + u].x;
+                d[u] = (i0 + u < n) ? __ldg(inq + off) : 0u;
+            }
+            unsigned ta, tb, fa, fb, e8;
+            csa(ta, ones, ones, d[0], d[1]);
+            csa(tb, ones, ones, d[2], d[3]);
+            csa(fa, twos, twos, ta, tb);
+            csa(ta, ones, ones, d[4], d[5]);
+            csa(tb, ones, ones, d[6], d[7]);
+            csa(fb, twos, twos, ta, tb);
+            csa(e8, fours, fours, fa, fb);
+            const unsigned c16 = eights & e8;
+            eights ^= e8;
+            thirtytwo |= sixteens & c16;
+            sixteens ^= c16;
+        }
+        // smallest count that could lift a row above -bias (0: every row may)
+        const float x = __fdiv_rd(reach, __uint_as_float(wmb));
+        const int Kt = !(x > 0.f) ? 0 : (x > 40.f ? 40 : (int)ceilf(x));
+        unsigned maybe;
+        {
+            const unsigned cs[6] = {ones, twos, fours, eights, sixteens, thirtytwo};
+            unsigned gt = 0u, eq = 0xffffffffu;
+#pragma unroll
+            for (int bit = 5; bit >= 0; --bit) {
+                const unsigned kb = ((Kt >> bit) & 1) ? 0xffffffffu : 0u;
+                gt |= eq & cs[bit] & ~kb;
+                eq &= ~(cs[bit] ^ kb);
+            }
+            maybe = tile_ok ? (gt | eq) : 0u;
+        }
+        const int cnt = __popc(maybe);
+        const int mcount = (int)__reduce_add_sync(0xffffffffu, (unsigned)cnt);
+        T v[SPL][RPL];
+        if (mcount == 0) {
+#pragma unroll
+            for (int g = 0; g < SPL; ++g)
+#pragma unroll
+                for (int c = 0; c < RPL; ++c) v[g][c] = T(0);
+        } else if (mcount <= kMaybeRows) {
+            // ---- list the maybe rows, one or two per lane
+            int pre = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int up = __shfl_up_sync(0xffffffffu, pre, o);
+                if (lane >= o) pre += up;
+            }
+            pre -= cnt;
+            for (unsigned mm = maybe; mm; mm &= mm - 1u) rows[pre++] = (unsigned short)(lane * 32 + __ffs(mm) - 1);
+            __syncwarp();
+            const bool two = mcount > 32;
+            const int ra = lane < mcount ? (int)rows[lane] : -1;
+            const int rb = (two && 32 + lane < mcount) ? (int)rows[32 + lane] : -1;
+            const unsigned* pa = inq0 + (max(ra, 0) >> 5);
+            const unsigned* pb = inq0 + (max(rb, 0) >> 5);
+            const unsigned sa = (unsigned)max(ra, 0) & 31u, sb = (unsigned)max(rb, 0) & 31u;
+            T xa = T(0), xb = T(0);
+            if (two) {
+#pragma unroll 4
+                for (int i = 0; i < n; ++i) {
+                    const unsigned off = wlist[i].x;
+                    const T w = wsm[i];
+                    const unsigned da = __ldg(pa + off), db = __ldg(pb + off);
+                    if ((da >> sa) & 1u) xa = A::add(xa, w);
+                    if ((db >> sb) & 1u) xb = A::add(xb, w);
+                }
+            } else {
+#pragma unroll 4
+                for (int i = 0; i < n; ++i) {
+                    const unsigned off = wlist[i].x;
+                    const T w = wsm[i];
+                    const unsigned da = __ldg(pa + off);
+                    if ((da >> sa) & 1u) xa = A::add(xa, w);
+                }
+            }
+            bool ka, kb;
+            const T va = bias_relu_clamp_keep(xa, L.bias, a.ymax, ka);
+            const T vb = bias_relu_clamp_keep(xb, L.bias, a.ymax, kb);
+            ka &= ra >= 0;
+            kb &= rb >= 0;
+            if (ka) stage[stage_pos<T>(ra >> 5, ra & 31)] = va;
+            if (kb) stage[stage_pos<T>(rb >> 5, rb & 31)] = vb;
+            __syncwarp();
+            // every lane reads back its own 32 rows (zero where nothing landed)
+            constexpr int EPC = 16 / (int)sizeof(T), CPR = 32 / EPC;
+            const uint4* srow = reinterpret_cast<const uint4*>(stage + lane * 32);
+#pragma unroll
+            for (int i = 0; i < CPR; ++i) {
+                uint4 u4 = make_uint4(0u, 0u, 0u, 0u);
+                if (maybe) u4 = srow[i ^ (lane & 7)];
+                const T* tv = reinterpret_cast<const T*>(&u4);
+#pragma unroll
+                for (int e = 0; e < EPC; ++e) v[(i * EPC + e) / RPL][(i * EPC + e) % RPL] = tv[e];
+            }
+            __syncwarp();
+            if (ka) stage[stage_pos<T>(ra >> 5, ra & 31)] = T(0);
+            if (kb) stage[stage_pos<T>(rb >> 5, rb & 31)] = T(0);
+        } else {
+            // ---- dense walk: every row of the word, one predicated add per set bit
+            T acc[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) acc[c] = T(0);
+            for (int i0 = 0; i0 < npad; i0 += GB) {
+                unsigned wd[GB];
+                T wv[GB];
+#pragma unroll
+                for (int u = 0; u < GB; ++u) {
+                    wd[u] = __ldg(inq + wlist[i0 + u].x);
+                    wv[u] = wsm[i0 + u];
+                }
+#pragma unroll
+                for (int u = 0; u < GB; ++u)
+#pragma unroll
+                    for (int c = 0; c < 32; ++c)
+                        if ((wd[u] >> c) & 1u) acc[c] = A::add(acc[c], wv[u]);
+            }
+#pragma unroll
+            for (int g = 0; g < SPL; ++g)
+#pragma unroll
+                for (int c = 0; c < RPL; ++c) {
+                    bool keep;
+                    v[g][c] = bias_relu_clamp_keep(acc[g * RPL + c], L.bias, a.ymax, keep);
+                }
+        }
+        alive32 |= quad_store<T>(v, out, ometa, cj, sub, tile_ok);
+        __syncwarp();  // the slot list and the row list are rewritten by the next column
+        cj += kWarps;
+        k0 = k1;
+        w0 = w1;
+        l0 = l1;
+        k1 = k2;
+        w1 = w2;
+    }
+    uint32_t* aw = a.alive + ((size_t)1 * a.n_tiles + t) * AW;
+    if (tile_ok && alive32) atomicOr(&aw[sub], alive32);
+    const unsigned any = __ballot_sync(0xffffffffu, tile_ok && alive32 != 0u);
+    constexpr unsigned kTileLanes = (1u << LPT) - 1u;
+    if (sub == 0 && ((any >> (LPT * T_)) & kTileLanes) && atomicOr(&aw[AW - 1], 1u) == 0u)
+        atomicAdd(&a.tile_count[1], 1);
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads, quad_occ<T>()) bin_quad_kernel(NetArgs<T> a) {
+    extern __shared__ __align__(16) unsigned char qsmem[];  // per warp: quad_warp_smem<T>() (prefilter only)
     __shared__ uint2 lists[kWarps][32];
     __shared__ long long s_item;
     if (a.stamps && blockIdx.x == 0 && threadIdx.x == 0) a.stamps[0] = globaltimer();
     if (__ldcg(&a.tile_count[0]) == 0) return;
     const LayerDesc<T> L = a.layers[0];
     constexpr int TPQ = quad_tiles<T>();
+    // the row prefilter needs one batch per column, a real epilogue and a negative bias
+    const bool pre = a.prefilter != 0 && a.epilogue != 0 && L.wp == 32 && L.bias < T(0);
+    unsigned char* wsmem = qsmem + (size_t)(threadIdx.x >> 5) * quad_warp_smem<T>();
+    if (pre) {  // the staging tile starts (and is kept) all zero
+        T* stage = reinterpret_cast<T*>(wsmem);
+        for (int i = threadIdx.x & 31; i < 1024; i += 32) stage[i] = T(0);
+        __syncwarp();
+    }
     const int nblk = (a.n_out + a.jb - 1) / a.jb;
     const long long items = (long long)((a.n_tiles + TPQ - 1) / TPQ) * nblk;
     for (;;) {
@@ -1415,7 +1712,10 @@ __global__ void __launch_bounds__(kThreads, quad_occ<T>()) bin_quad_kernel(NetAr
         if (it >= items) break;
         const int q = (int)(it / nblk), bb = (int)(it % nblk);
         const int j0 = bb * a.jb, j1 = min(a.n_out, j0 + a.jb);
-        bin_quad_item<T, SDNN_QUAD_GB>(a, L, q, j0, j1, lists[threadIdx.x >> 5]);
+        if (pre)
+            bin_quad_item1<T, SDNN_QUAD_GB>(a, L, q, j0, j1, lists[threadIdx.x >> 5], wsmem);
+        else
+            bin_quad_item<T, SDNN_QUAD_GB>(a, L, q, j0, j1, lists[threadIdx.x >> 5]);
     }
 }
 
