@@ -136,6 +136,7 @@ struct sdnn_net {
     uint32_t* alive_c = nullptr;   // row bitmaps of repacked tiles
     int64_t accap = 0;
     int* n_compact = nullptr;
+    int* probe_flag = nullptr;  // layer-1 walk chosen by quad_probe_kernel
     int32_t* tile_count = nullptr;
     int64_t* live_rows = nullptr;
     unsigned long long* stamps = nullptr;
@@ -755,14 +756,27 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     }
     CK(cudaEventRecord(net->ev_d, net->stream));
     if (a.bin_in && quad) {  // layer 1 over quad / oct bit-lines: its own launch
-        const void* qfn = (const void*)bin_quad_kernel<T>;
+        // dense walk, or -- when a device-side probe of sampled columns says few
+        // rows can reach -bias -- the row-prefilter walk (SDNN_PREFILTER=0: never);
+        // both variants are launched, the one the probe's flag does not name returns
+        const bool pre = a.prune && env_int("SDNN_PREFILTER", 1) != 0;
+        const void* qfn = (const void*)bin_quad_kernel<T, false>;
         int qocc = 0;
-        // row prefilter (SDNN_PREFILTER=0 turns it off): per-warp staging tile in dynamic shared memory
-        a.prefilter = a.prune ? env_int("SDNN_PREFILTER", 1) : 0;
-        const size_t qsmem = a.prefilter ? (size_t)kWarps * quad_warp_smem<T>() : 0;
-        CK(cudaFuncSetAttribute(qfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsmem));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&qocc, qfn, kThreads, qsmem));
-        bin_quad_kernel<T><<<net->sm_count * std::max(qocc, 1), kThreads, qsmem, net->stream>>>(a);
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&qocc, qfn, kThreads, 0));
+        int* flag = nullptr;
+        if (pre) {
+            if (!net->probe_flag) CK(cudaMalloc(&net->probe_flag, 4));
+            flag = net->probe_flag;
+            quad_probe_kernel<T><<<1, kThreads, 0, net->stream>>>(a, flag);
+            const void* pfn = (const void*)bin_quad_kernel<T, true>;
+            const size_t qsmem = (size_t)kWarps * quad_warp_smem<T>();
+            CK(cudaFuncSetAttribute(pfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsmem));
+            int pocc = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pocc, pfn, kThreads, qsmem));
+            bin_quad_kernel<T, true><<<net->sm_count * std::max(pocc, 1), kThreads, qsmem, net->stream>>>(a, flag);
+            res->launches += 2;
+        }
+        bin_quad_kernel<T, false><<<net->sm_count * std::max(qocc, 1), kThreads, 0, net->stream>>>(a, flag);
         CK(cudaGetLastError());
         res->launches += 1;
         a.first_l = 1;
@@ -1509,6 +1523,7 @@ void sdnn_net_destroy(sdnn_net* net) {
     cudaFree(net->rowid_alt);
     cudaFree(net->alive_c);
     cudaFree(net->n_compact);
+    cudaFree(net->probe_flag);
     cudaFree(net->rowlist);
     cudaFree(net->live_rows);
     cudaFree(net->stamps);

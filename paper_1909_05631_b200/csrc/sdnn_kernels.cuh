@@ -296,8 +296,6 @@ struct NetArgs {
     // margin) is all zero after the epilogue and gathers nothing
     int prune;
     unsigned* pruned;     // [L] (tile, output) columns pruned per layer, or null
-    int prefilter;        // layer 1 over quad/oct bit-lines: exact chains only for rows whose set-input
-                          // count could reach -bias (bin_quad_item1)
 };
 constexpr int kDensitySample = 256;  // input lines sampled per layer (the same ones in every CTA)
 
@@ -1411,15 +1409,52 @@ __device__ __forceinline__ void bin_quad_item(const NetArgs<T>& a, const LayerDe
 // load per slot, the same ascending order and the same additions as the
 // dense walk, so the same bits), applies the epilogue and drops the value
 // into the warp's staging tile, from which every lane reads back its own 32
-// rows for the usual sector stores.  Columns with more than 64 maybe rows take
-// the dense walk.  Exact: the count bound only ever errs towards "maybe"
+// rows for the usual sector stores.  Whether the launch takes this walk or
+// the dense one (bin_quad_item) is decided on the device by quad_probe_kernel
+// from the maybe rows of sampled columns.  Exact: the count bound only ever errs towards "maybe"
 // (weights rounded up, -bias scaled by 1 - 2^-10 and rounded down).
 __device__ __forceinline__ void csa(unsigned& h, unsigned& l, unsigned x, unsigned y, unsigned z) {
     const unsigned u = x ^ y;
     h = (x & y) | (u & z);
     l = u ^ z;
 }
-constexpr int kMaybeRows = 64;  // listed rows per column (two per lane)
+// Rows (bits) of this lane's 32-row word whose count of set inputs over the
+// column's live slots (d[i], zero beyond them) could reach -bias: the counts
+// come from a bit-sliced carry-save tree, Kt = the smallest count with
+// Kt * wmax >= reach (reach = -bias * (1 - 2^-10) rounded down, wmax the
+// column's largest |weight| rounded up; 0: every row may), the compare is
+// bit-sliced too.
+__device__ __forceinline__ unsigned maybe_mask(const unsigned (&d)[32], unsigned wmax_bits, float reach) {
+    unsigned ones = 0u, twos = 0u, fours = 0u, eights = 0u, sixteens = 0u, thirtytwo = 0u;
+#pragma unroll
+    for (int i0 = 0; i0 < 32; i0 += 8) {
+        unsigned ta, tb, fa, fb, e8;
+        csa(ta, ones, ones, d[i0 + 0], d[i0 + 1]);
+        csa(tb, ones, ones, d[i0 + 2], d[i0 + 3]);
+        csa(fa, twos, twos, ta, tb);
+        csa(ta, ones, ones, d[i0 + 4], d[i0 + 5]);
+        csa(tb, ones, ones, d[i0 + 6], d[i0 + 7]);
+        csa(fb, twos, twos, ta, tb);
+        csa(e8, fours, fours, fa, fb);
+        const unsigned c16 = eights & e8;
+        eights ^= e8;
+        thirtytwo |= sixteens & c16;
+        sixteens ^= c16;
+    }
+    const float x = __fdiv_rd(reach, __uint_as_float(wmax_bits));
+    const int Kt = !(x > 0.f) ? 0 : (x > 40.f ? 40 : (int)ceilf(x));
+    const unsigned cs[6] = {ones, twos, fours, eights, sixteens, thirtytwo};
+    unsigned gt = 0u, eq = 0xffffffffu;
+#pragma unroll
+    for (int bit = 5; bit >= 0; --bit) {
+        const unsigned kb = ((Kt >> bit) & 1) ? 0xffffffffu : 0u;
+        gt |= eq & cs[bit] & ~kb;
+        eq &= ~(cs[bit] ^ kb);
+    }
+    return gt | eq;
+}
+
+constexpr int kMaybeRows = 1024;  // row list capacity: every row of the quad
 template <typename T>
 __host__ __device__ constexpr int quad_warp_smem() {  // staging tile + weights + row list, per warp
     return 1024 * (int)sizeof(T) + 32 * (int)sizeof(T) + kMaybeRows * 2;
@@ -1464,6 +1499,44 @@ __device__ __forceinline__ unsigned quad_store(const T (&v)[32 / rows_per_lane<T
         if (sub == 0) ometa[cj] = make_uint2(m, ob);
     }
     return bits32;
+}
+
+// Exact chains of up to R listed rows per lane (rows[i], rows[32 + i], ...:
+// word = row >> 5, bit = row & 31).  d[i] is this lane's word of the
+// column's i-th live slot (kept in registers by the count pass); the word
+// of another lane's row comes by shuffle, so the walk touches no memory but
+// the slot's weight: the live slots in list order, the same additions as
+// the dense walk.  Then the epilogue; kept values go to the staging tile.
+template <typename T, int R>
+__device__ __forceinline__ void maybe_chains(const unsigned (&d)[32], const T* wsm, int n, const unsigned short* rows,
+                                             int mcount, T* stage, T bias, T ymax) {
+    const int lane = threadIdx.x & 31;
+    int r[R], wi[R];
+    unsigned sh[R];
+    T x[R];
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+        r[u] = u * 32 + lane < mcount ? (int)rows[u * 32 + lane] : -1;
+        wi[u] = max(r[u], 0) >> 5;
+        sh[u] = (unsigned)max(r[u], 0) & 31u;
+        x[u] = T(0);
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        if (i >= n) break;
+        const T w = wsm[i];
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+            const unsigned dd = __shfl_sync(0xffffffffu, d[i], wi[u]);
+            if ((dd >> sh[u]) & 1u) x[u] = Arith<T>::add(x[u], w);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+        bool keep;
+        const T val = bias_relu_clamp_keep(x[u], bias, ymax, keep);
+        if (keep && r[u] >= 0) stage[stage_pos<T>(r[u] >> 5, r[u] & 31)] = val;
+    }
 }
 
 template <typename T, int GB>
@@ -1538,53 +1611,25 @@ __device__ __forceinline__ void bin_quad_item1(const NetArgs<T>& a, const LayerD
         }
         const unsigned wmb = __reduce_max_sync(0xffffffffu, l0 ? __float_as_uint(bound_up(w0)) : 0u);
         __syncwarp();
-        // ---- count the set inputs of every row (bit-sliced, 8 slots a round)
-        unsigned ones = 0u, twos = 0u, fours = 0u, eights = 0u, sixteens = 0u, thirtytwo = 0u;
-        for (int i0 = 0; i0 < n; i0 += 8) {
-            unsigned d[8];
+        T v[SPL][RPL];
+        // ---- count the set inputs of every row, bit-sliced: this lane's word of
+        // every live slot (all loads in flight at once), then a carry-save tree
+        unsigned d[32];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const unsigned off = wlist[i0 + u].x;
-                d[u] = (i0 + u < n) ? __ldg(inq + off) : 0u;
-            }
-            unsigned ta, tb, fa, fb, e8;
-            csa(ta, ones, ones, d[0], d[1]);
-            csa(tb, ones, ones, d[2], d[3]);
-            csa(fa, twos, twos, ta, tb);
-            csa(ta, ones, ones, d[4], d[5]);
-            csa(tb, ones, ones, d[6], d[7]);
-            csa(fb, twos, twos, ta, tb);
-            csa(e8, fours, fours, fa, fb);
-            const unsigned c16 = eights & e8;
-            eights ^= e8;
-            thirtytwo |= sixteens & c16;
-            sixteens ^= c16;
+        for (int i = 0; i < 32; ++i) {
+            const unsigned off = wlist[i].x;
+            d[i] = (i < n) ? __ldg(inq + off) : 0u;
         }
-        // smallest count that could lift a row above -bias (0: every row may)
-        const float x = __fdiv_rd(reach, __uint_as_float(wmb));
-        const int Kt = !(x > 0.f) ? 0 : (x > 40.f ? 40 : (int)ceilf(x));
-        unsigned maybe;
-        {
-            const unsigned cs[6] = {ones, twos, fours, eights, sixteens, thirtytwo};
-            unsigned gt = 0u, eq = 0xffffffffu;
-#pragma unroll
-            for (int bit = 5; bit >= 0; --bit) {
-                const unsigned kb = ((Kt >> bit) & 1) ? 0xffffffffu : 0u;
-                gt |= eq & cs[bit] & ~kb;
-                eq &= ~(cs[bit] ^ kb);
-            }
-            maybe = tile_ok ? (gt | eq) : 0u;
-        }
+        const unsigned maybe = tile_ok ? maybe_mask(d, wmb, reach) : 0u;
         const int cnt = __popc(maybe);
         const int mcount = (int)__reduce_add_sync(0xffffffffu, (unsigned)cnt);
-        T v[SPL][RPL];
         if (mcount == 0) {
 #pragma unroll
             for (int g = 0; g < SPL; ++g)
 #pragma unroll
                 for (int c = 0; c < RPL; ++c) v[g][c] = T(0);
-        } else if (mcount <= kMaybeRows) {
-            // ---- list the maybe rows, one or two per lane
+        } else {
+            // ---- list the maybe rows; lane i takes rows i, 32 + i, ... of the list
             int pre = cnt;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -1594,38 +1639,15 @@ __device__ __forceinline__ void bin_quad_item1(const NetArgs<T>& a, const LayerD
             pre -= cnt;
             for (unsigned mm = maybe; mm; mm &= mm - 1u) rows[pre++] = (unsigned short)(lane * 32 + __ffs(mm) - 1);
             __syncwarp();
-            const bool two = mcount > 32;
-            const int ra = lane < mcount ? (int)rows[lane] : -1;
-            const int rb = (two && 32 + lane < mcount) ? (int)rows[32 + lane] : -1;
-            const unsigned* pa = inq0 + (max(ra, 0) >> 5);
-            const unsigned* pb = inq0 + (max(rb, 0) >> 5);
-            const unsigned sa = (unsigned)max(ra, 0) & 31u, sb = (unsigned)max(rb, 0) & 31u;
-            T xa = T(0), xb = T(0);
-            if (two) {
-#pragma unroll 4
-                for (int i = 0; i < n; ++i) {
-                    const unsigned off = wlist[i].x;
-                    const T w = wsm[i];
-                    const unsigned da = __ldg(pa + off), db = __ldg(pb + off);
-                    if ((da >> sa) & 1u) xa = A::add(xa, w);
-                    if ((db >> sb) & 1u) xb = A::add(xb, w);
-                }
-            } else {
-#pragma unroll 4
-                for (int i = 0; i < n; ++i) {
-                    const unsigned off = wlist[i].x;
-                    const T w = wsm[i];
-                    const unsigned da = __ldg(pa + off);
-                    if ((da >> sa) & 1u) xa = A::add(xa, w);
-                }
+            switch ((mcount + 31) >> 5) {
+                case 1: maybe_chains<T, 1>(d, wsm, n, rows, mcount, stage, L.bias, a.ymax); break;
+                case 2: maybe_chains<T, 2>(d, wsm, n, rows, mcount, stage, L.bias, a.ymax); break;
+                case 3: maybe_chains<T, 3>(d, wsm, n, rows, mcount, stage, L.bias, a.ymax); break;
+                default:  // four rows per lane a pass, as many passes as the list needs
+                    for (int base = 0; base < mcount; base += 128)
+                        maybe_chains<T, 4>(d, wsm, n, rows + base, mcount - base, stage, L.bias, a.ymax);
+                    break;
             }
-            bool ka, kb;
-            const T va = bias_relu_clamp_keep(xa, L.bias, a.ymax, ka);
-            const T vb = bias_relu_clamp_keep(xb, L.bias, a.ymax, kb);
-            ka &= ra >= 0;
-            kb &= rb >= 0;
-            if (ka) stage[stage_pos<T>(ra >> 5, ra & 31)] = va;
-            if (kb) stage[stage_pos<T>(rb >> 5, rb & 31)] = vb;
             __syncwarp();
             // every lane reads back its own 32 rows (zero where nothing landed)
             constexpr int EPC = 16 / (int)sizeof(T), CPR = 32 / EPC;
@@ -1639,34 +1661,11 @@ __device__ __forceinline__ void bin_quad_item1(const NetArgs<T>& a, const LayerD
                 for (int e = 0; e < EPC; ++e) v[(i * EPC + e) / RPL][(i * EPC + e) % RPL] = tv[e];
             }
             __syncwarp();
-            if (ka) stage[stage_pos<T>(ra >> 5, ra & 31)] = T(0);
-            if (kb) stage[stage_pos<T>(rb >> 5, rb & 31)] = T(0);
-        } else {
-            // ---- dense walk: every row of the word, one predicated add per set bit
-            T acc[32];
-#pragma unroll
-            for (int c = 0; c < 32; ++c) acc[c] = T(0);
-            for (int i0 = 0; i0 < npad; i0 += GB) {
-                unsigned wd[GB];
-                T wv[GB];
-#pragma unroll
-                for (int u = 0; u < GB; ++u) {
-                    wd[u] = __ldg(inq + wlist[i0 + u].x);
-                    wv[u] = wsm[i0 + u];
-                }
-#pragma unroll
-                for (int u = 0; u < GB; ++u)
-#pragma unroll
-                    for (int c = 0; c < 32; ++c)
-                        if ((wd[u] >> c) & 1u) acc[c] = A::add(acc[c], wv[u]);
+            // the staging tile goes back to all zero
+            for (int i = lane; i < mcount; i += 32) {
+                const int r = (int)rows[i];
+                stage[stage_pos<T>(r >> 5, r & 31)] = T(0);
             }
-#pragma unroll
-            for (int g = 0; g < SPL; ++g)
-#pragma unroll
-                for (int c = 0; c < RPL; ++c) {
-                    bool keep;
-                    v[g][c] = bias_relu_clamp_keep(acc[g * RPL + c], L.bias, a.ymax, keep);
-                }
         }
         alive32 |= quad_store<T>(v, out, ometa, cj, sub, tile_ok);
         __syncwarp();  // the slot list and the row list are rewritten by the next column
@@ -1685,19 +1684,78 @@ __device__ __forceinline__ void bin_quad_item1(const NetArgs<T>& a, const LayerD
         atomicAdd(&a.tile_count[1], 1);
 }
 
+// Samples 32 (quad, column) pairs of layer 1 and counts their maybe rows:
+// *flag = 1 (row-prefilter walk) when they average at most `limit` of 1,024
+// rows, else 0 (dense walk).  One CTA; the two bin_quad_kernel variants are
+// both launched and the one the flag does not name returns at once.
+// Measured crossover (C4 rows, 6 % maybe rows = 64 per column: float dense
+// 5.04 ms vs prefilter 5.66 ms, double 12.3 vs 8.6 ms; C5 p = 0.1, ~0 maybe
+// rows: float 4.70 vs 3.20 ms): the float dense walk's 32 predicated adds
+// per slot issue so well that listing rows only pays below ~32 a column;
+// the double dense walk is bound by the FP64 pipe and loses up to ~160.
 template <typename T>
-__global__ void __launch_bounds__(kThreads, quad_occ<T>()) bin_quad_kernel(NetArgs<T> a) {
-    extern __shared__ __align__(16) unsigned char qsmem[];  // per warp: quad_warp_smem<T>() (prefilter only)
+__host__ __device__ constexpr int prefilter_limit() { return sizeof(T) == 4 ? 32 : 160; }
+template <typename T>
+__global__ void __launch_bounds__(kThreads) quad_probe_kernel(NetArgs<T> a, int* flag) {
+    constexpr int TPQ = quad_tiles<T>(), LPT = 32 / TPQ;
+    __shared__ int s_sum[kWarps];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const LayerDesc<T> L = a.layers[0];
+    const int n_quads = (a.n_tiles + TPQ - 1) / TPQ;
+    int sum = 0;
+    const bool ok = a.epilogue != 0 && L.wp == 32 && L.bias < T(0) && n_quads > 0 && a.n_out > 0;
+    if (ok) {
+        const float reach = __fmul_rd(-bias_toward_zero(L.bias), 0.9990234375f);
+        for (int smp = warp; smp < 32; smp += kWarps) {
+            const int q = (int)(((unsigned)smp * 2654435761u >> 8) % (unsigned)n_quads);
+            const int j = (int)(((unsigned)smp * 40503u + 17u) * 2246822519u % (unsigned)a.n_out);
+            const int ntq = min(TPQ, a.n_tiles - q * TPQ);
+            const bool tile_ok = lane / LPT < ntq;
+            const unsigned* inq = reinterpret_cast<const unsigned*>(reinterpret_cast<const char*>(a.slab[0]) +
+                                                                    (size_t)q * a.ld * kQuadLine) + lane;
+            const uint2* m0p = a.meta[0] + (size_t)q * a.ld;
+            const int k = L.idx[(size_t)j * 32 + lane];
+            const T w = L.val[(size_t)j * 32 + lane];
+            const bool live = k >= 0 && m0p[k].x != 0u;
+            const unsigned wmb = __reduce_max_sync(0xffffffffu, live ? __float_as_uint(bound_up(w)) : 0u);
+            unsigned d[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const int ki = __shfl_sync(0xffffffffu, live ? k : -1, i);
+                d[i] = ki >= 0 ? __ldg(inq + (size_t)ki * (kQuadLine / 4)) : 0u;
+            }
+            const unsigned maybe = tile_ok ? maybe_mask(d, wmb, reach) : 0u;
+            sum += (int)__reduce_add_sync(0xffffffffu, (unsigned)__popc(maybe));
+        }
+    }
+    if (lane == 0) s_sum[warp] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int tot = 0;
+        for (int i = 0; i < kWarps; ++i) tot += s_sum[i];
+        *flag = (ok && tot <= prefilter_limit<T>() * 32) ? 1 : 0;
+    }
+}
+
+// PRE: the row-prefilter walk (bin_quad_item1), run when *flag == 1; else the
+// dense walk, run when flag is null or *flag == 0.
+#ifndef SDNN_PRE_OCC
+#define SDNN_PRE_OCC 2  // float row-prefilter walk: 32 slot words in registers
+#endif
+template <typename T, bool PRE>
+__host__ __device__ constexpr int quad_kernel_occ() { return (PRE && sizeof(T) == 4) ? SDNN_PRE_OCC : quad_occ<T>(); }
+template <typename T, bool PRE>
+__global__ void __launch_bounds__(kThreads, quad_kernel_occ<T, PRE>()) bin_quad_kernel(NetArgs<T> a, const int* flag) {
+    extern __shared__ __align__(16) unsigned char qsmem[];  // PRE: per warp quad_warp_smem<T>()
     __shared__ uint2 lists[kWarps][32];
     __shared__ long long s_item;
+    if (flag && (__ldcg(flag) != 0) != PRE) return;
     if (a.stamps && blockIdx.x == 0 && threadIdx.x == 0) a.stamps[0] = globaltimer();
     if (__ldcg(&a.tile_count[0]) == 0) return;
     const LayerDesc<T> L = a.layers[0];
     constexpr int TPQ = quad_tiles<T>();
-    // the row prefilter needs one batch per column, a real epilogue and a negative bias
-    const bool pre = a.prefilter != 0 && a.epilogue != 0 && L.wp == 32 && L.bias < T(0);
     unsigned char* wsmem = qsmem + (size_t)(threadIdx.x >> 5) * quad_warp_smem<T>();
-    if (pre) {  // the staging tile starts (and is kept) all zero
+    if (PRE) {  // the staging tile starts (and is kept) all zero
         T* stage = reinterpret_cast<T*>(wsmem);
         for (int i = threadIdx.x & 31; i < 1024; i += 32) stage[i] = T(0);
         __syncwarp();
@@ -1712,7 +1770,7 @@ __global__ void __launch_bounds__(kThreads, quad_occ<T>()) bin_quad_kernel(NetAr
         if (it >= items) break;
         const int q = (int)(it / nblk), bb = (int)(it % nblk);
         const int j0 = bb * a.jb, j1 = min(a.n_out, j0 + a.jb);
-        if (pre)
+        if constexpr (PRE)
             bin_quad_item1<T, SDNN_QUAD_GB>(a, L, q, j0, j1, lists[threadIdx.x >> 5], wsmem);
         else
             bin_quad_item<T, SDNN_QUAD_GB>(a, L, q, j0, j1, lists[threadIdx.x >> 5]);

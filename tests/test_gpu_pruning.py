@@ -147,3 +147,37 @@ def test_rounding_boundary(dtype, prec):
         assert O.CSR(rows, n, *on.y).identical(want), bias
         assert (on.categories.size == rows) == survive, bias
         net.close()
+
+
+@pytest.mark.parametrize("dtype,prec", [("f32", 32), ("f64", 64)])
+@pytest.mark.parametrize("scale,bias", [(0.06, -0.45), (0.11, -0.45), (0.2, -0.1)])
+def test_layer1_prefilter_with_uneven_weights(monkeypatch, dtype, prec, scale, bias):
+    """Layer 1 over bit-lines with the row prefilter (bin_quad_item1): the
+    count bound uses the column's largest |weight|, so uneven and mixed-sign
+    weights only make it looser, never wrong.  scale 0.06: few rows pass the
+    count test (listed rows, exact chains); 0.11: some columns list rows and
+    some take the dense walk; 0.2 with a small bias: every row passes.
+    Prefilter on == prefilter off == oracle, bit for bit."""
+    n, rows, layers = 1024, 3000, 3
+    w = W.Workload("t", n, layers, rows, 32, 20, 0.35, bias, value=scale)
+    off, cols, vals = W.images(w)
+    y0 = O.CSR(rows, n, off, cols, vals)
+    rng = np.random.default_rng(int(scale * 1000))
+    lw = []
+    for l in range(layers):
+        o, c, v = W.layer_csr(w, l)
+        v = rng.uniform(0.3 * scale, scale, v.shape) * np.where(rng.random(v.shape) < 0.15, -1.0, 1.0)
+        lw.append(O.CSR(n, n, o, c, v))
+    want = O.infer(lw, [bias] * layers, y0, w.ymax, precision=prec, threads=8)
+    net = E.DeviceNetwork(n, 0, dtype)
+    for m in lw:
+        net.add_layer_csr(sm(m), bias)
+    batch = net.upload_csr(rows, off, cols, vals)
+    outs = []
+    for pre in ("1", "0"):
+        monkeypatch.setenv("SDNN_PREFILTER", pre)
+        r = net.run(batch, w.ymax, want_y=True)
+        assert O.CSR(rows, n, *r.y).identical(want), (pre, dtype)
+        outs.append(r)
+    assert np.array_equal(outs[0].live_rows, outs[1].live_rows)
+    net.close()
