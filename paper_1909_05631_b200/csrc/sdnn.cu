@@ -137,6 +137,8 @@ struct sdnn_net {
     int64_t accap = 0;
     int* n_compact = nullptr;
     int* probe_flag = nullptr;  // layer-1 walk chosen by quad_probe_kernel
+    uint32_t* prune_map = nullptr;  // prune pass: one bit per (tile, output)
+    int64_t pmcap = 0;
     int32_t* tile_count = nullptr;
     int64_t* live_rows = nullptr;
     unsigned long long* stamps = nullptr;
@@ -633,7 +635,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
         if (int rc = grow(net->tile_count, c1, nl + 1, 4)) return rc;
         if (int rc = grow(net->live_rows, c2, nl + 1, 8)) return rc;
         if (int rc = grow(net->stamps, c3, nl + 1, 8)) return rc;
-        if (int rc = grow(net->work, c4, 3 * (nl + 1), 4)) return rc;  // layers, compactions, pruned columns
+        if (int rc = grow(net->work, c4, 4 * (nl + 1), 4)) return rc;  // layers, compactions, pruned columns, prune pass
         net->lcap = nl + 1;
     }
     int32_t* tile_count = net->tile_count;
@@ -652,7 +654,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     uint32_t* heap = net->heap;
     CK(cudaMemsetAsync(heap, 0, (nl + 1) * tiles1 * 4, net->stream));
     unsigned* work = net->work;
-    CK(cudaMemsetAsync(work, 0, 3 * (nl + 1) * 4, net->stream));
+    CK(cudaMemsetAsync(work, 0, 4 * (nl + 1) * 4, net->stream));
     if (int rc = grow(net->alive_c, net->accap, tiles1 * AW, 4)) return rc;
     if (!net->n_compact) CK(cudaMalloc(&net->n_compact, 4));
     CK(cudaMemsetAsync(net->n_compact, 0, 4, net->stream));
@@ -690,6 +692,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     // output pruning by line bounds (sdnn_net_set_pruning; SDNN_PRUNE=0 turns it off)
     a.prune = epilogue ? env_int("SDNN_PRUNE", net->prune) : 0;  // raw Z (engine.spmm) keeps every entry
     a.pruned = work + 2 * (nl + 1);
+    a.pp_work = work + 3 * (nl + 1);
     a.jb = env_int("SDNN_JB", net->jb);
     // dense inputs (>= 60 % of sectors kept): 64-output items -- measured on
     // the K2 companion's dense layers, 36.7 -> 29.9 ms at JB 256 -> 64; C4's
@@ -709,7 +712,24 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
 #endif
     const void* fn = zfill ? (const void*)net_kernel<T, SDNN_NET_GB, true>
                            : (const void*)net_kernel<T, SDNN_NET_GB, false>;
-    const size_t smem = (size_t)(2 * tiles1 + 1) * 4;  // live-tile list + row prefix
+    size_t smem = (size_t)(2 * tiles1 + 1) * 4;  // live-tile list + row prefix
+    const size_t smem_list = smem;
+    {
+        // prune pass: n_in bytes of bound codes behind the tile list, when that
+        // keeps the kernel's CTAs per SM (SDNN_PRUNE_PASS=0: never)
+        const size_t pp_off = (smem + 15) / 16 * 16, with = pp_off + (size_t)n_in;
+        int occ0 = 0, occ1 = 0;
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::min<size_t>(with, 200 << 10)));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ0, fn, kThreads, smem));
+        if (with <= (200u << 10)) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, fn, kThreads, with));
+        if (a.prune && env_int("SDNN_PRUNE_PASS", 1) != 0 && occ1 >= 1 && occ1 == occ0) {
+            if (int rc = grow(net->prune_map, net->pmcap, tiles1 * ((ld + 31) / 32), 4)) return rc;
+            a.prune_pass = 1;
+            a.pp_off = (int)pp_off;
+            a.prune_map = net->prune_map;
+            smem = with;
+        }
+    }
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem));
@@ -767,7 +787,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
         if (pre) {
             if (!net->probe_flag) CK(cudaMalloc(&net->probe_flag, 4));
             flag = net->probe_flag;
-            quad_probe_kernel<T><<<1, kThreads, 0, net->stream>>>(a, flag);
+            quad_probe_kernel<T><<<1, kThreads, 0, net->stream>>>(a, flag, env_int("SDNN_PREFILTER", 1) == 2);
             const void* pfn = (const void*)bin_quad_kernel<T, true>;
             const size_t qsmem = (size_t)kWarps * quad_warp_smem<T>();
             CK(cudaFuncSetAttribute(pfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsmem));
@@ -782,10 +802,10 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
         a.first_l = 1;
     } else if (a.bin_in) {  // layer 1 over bit-line tiles: its own launch
         const void* bfn = (const void*)bin_layer_kernel<T>;
-        CK(cudaFuncSetAttribute(bfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(bfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_list));
         int bocc = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bocc, bfn, kThreads, smem));
-        bin_layer_kernel<T><<<net->sm_count * std::max(bocc, 1), kThreads, smem, net->stream>>>(a);
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bocc, bfn, kThreads, smem_list));
+        bin_layer_kernel<T><<<net->sm_count * std::max(bocc, 1), kThreads, smem_list, net->stream>>>(a);
         CK(cudaGetLastError());
         res->launches += 1;
         a.first_l = 1;
@@ -1524,6 +1544,7 @@ void sdnn_net_destroy(sdnn_net* net) {
     cudaFree(net->alive_c);
     cudaFree(net->n_compact);
     cudaFree(net->probe_flag);
+    cudaFree(net->prune_map);
     cudaFree(net->rowlist);
     cudaFree(net->live_rows);
     cudaFree(net->stamps);

@@ -296,6 +296,12 @@ struct NetArgs {
     // margin) is all zero after the epilogue and gathers nothing
     int prune;
     unsigned* pruned;     // [L] (tile, output) columns pruned per layer, or null
+    // prune pass (sparse layers): a tile's line bounds as 8-bit codes in shared
+    // memory, every column of the tile tested against them, one bit a column
+    int prune_pass;       // 1: the launch has room for the codes (n_in bytes of dynamic shared memory)
+    int pp_off;           // byte offset of the codes in dynamic shared memory
+    uint32_t* prune_map;  // [n_tiles][(ld + 31) / 32] bit j: column j of the tile is pruned
+    unsigned* pp_work;    // [L] work-item counters of the pass
 };
 constexpr int kDensitySample = 256;  // input lines sampled per layer (the same ones in every CTA)
 
@@ -648,7 +654,8 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_bin_kernel(const int6
 // every value the kernel can read is finite (Y0 finite and ymax finite).
 template <typename T, int GB, bool BIN, bool ZFILL>
 __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<T>& L, int l, bool odd, int t,
-                                           int j0, int j1, SlotEntry<T>* wlist) {
+                                           int j0, int j1, SlotEntry<T>* wlist, const uint32_t* pmap,
+                                           unsigned char* wcols) {
     using A = Arith<T>;
     constexpr int RPL = rows_per_lane<T>(), AW = alive_words<T>();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -669,22 +676,50 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
     if (jw >= j1) return;
     const int nb = L.wp / 32;  // batches per column
     const int n_cols = (j1 - jw + kWarps - 1) / kWarps;
-    const int total = n_cols * nb;
+    int total = n_cols * nb;
     if (total == 0) {  // zero-width layer: every output is an empty chain
         for (int j = jw; j < j1; j += kWarps)
             if (lane == 0) ometa[j] = make_uint2(0u, 0u);
         return;
     }
+    unsigned alive_bits = 0u;  // row bits of the lane; pruned columns are counted above bit 16
+    // map mode: the prune pass left one bit per column of this tile.  Lane i
+    // looks up the warp's column i; pruned columns get their empty meta here
+    // and the walk below visits only the others, through the warp's list of
+    // remaining column numbers (no slot, meta or line is read for a pruned one)
+    const bool map_mode = !BIN && pmap != nullptr && nb == 1 && n_cols <= 32;
+    if (map_mode) {
+        const int ci = jw + kWarps * lane;
+        const bool mine = lane < n_cols;
+        const bool pr = mine && ((__ldg(&pmap[ci >> 5]) >> (ci & 31)) & 1u);
+        const unsigned pm = __ballot_sync(0xffffffffu, pr);
+        const unsigned todo = __ballot_sync(0xffffffffu, mine && !pr);
+        if (pr) ometa[ci] = make_uint2(0u, 0u);
+        if (mine && !pr) wcols[__popc(todo & below)] = (unsigned char)lane;
+        __syncwarp();
+        alive_bits = (unsigned)__popc(pm) << 16;
+        total = __popc(todo);
+        if (total == 0) {
+            if (a.pruned && lane == 0) atomicAdd(&a.pruned[l], alive_bits >> 16);
+            return;
+        }
+    }
     // slot cursor of the next batch to prefetch: columns jw, jw + kWarps, ...
-    // each nb batches of 32 slots (no divisions in the loop)
-    size_t po = (size_t)jw * L.wp + lane;
-    int pb = 0;
+    // each nb batches of 32 slots (no divisions in the loop); map mode: the
+    // listed columns, one batch each, pb counting list entries
+    size_t po = (size_t)(map_mode ? jw + kWarps * (int)wcols[0] : jw) * L.wp + lane;
+    int pb = map_mode ? 1 : 0;
     const size_t col_skip = (size_t)(kWarps - 1) * L.wp;
     auto advance = [&]() {
-        po += 32;
-        if (++pb == nb) {
-            pb = 0;
-            po += col_skip;
+        if (map_mode) {
+            po = (size_t)(jw + kWarps * (int)wcols[pb & 31]) * 32 + lane;
+            ++pb;
+        } else {
+            po += 32;
+            if (++pb == nb) {
+                pb = 0;
+                po += col_skip;
+            }
         }
     };
     // pipeline registers: (k1, w1) for batch b+1, (k2, w2) for batch b+2
@@ -701,7 +736,6 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
     }
     uint2 m0 = k0 >= 0 ? imeta[k0] : make_uint2(0u, 0u);
     T acc[RPL];
-    unsigned alive_bits = 0u;
 #pragma unroll
     for (int c = 0; c < RPL; ++c) acc[c] = T(0);
     // gather registers (loop-carried: without ZFILL a dead lane keeps them)
@@ -712,7 +746,7 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
 #pragma unroll
         for (int c = 0; c < RPL; ++c) ya[u][c] = yb[u][c] = T(0);
     }
-    int cj = jw, cb = 0;  // current column and batch within it
+    int cj = map_mode ? jw + kWarps * (int)wcols[0] : jw, cb = 0;  // current column and batch within it
     for (int b = 0; b < total; ++b) {
         // issue the next loads before working on batch b
         if (b + 2 < total) {
@@ -739,7 +773,7 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
                 // still zero, nothing to list, gather or store but the meta
                 alive_bits += 0x10000u;  // pruned columns are counted above the row bits
                 if (lane == 0) ometa[cj] = make_uint2(0u, 0u);
-                cj += kWarps;
+                cj = map_mode ? jw + kWarps * (int)wcols[(b + 1) & 31] : cj + kWarps;
                 k0 = k1;
                 w0 = w1;
                 m0 = m1;
@@ -872,7 +906,7 @@ __device__ __forceinline__ void layer_item(const NetArgs<T>& a, const LayerDesc<
             const unsigned ob = om ? __reduce_max_sync(0xffffffffu, lane_bound(v)) : 0u;
             if (lane == 0) ometa[cj] = make_uint2(om, ob);
             alive_bits |= bits;
-            cj += kWarps;
+            cj = map_mode ? jw + kWarps * (int)wcols[(b + 1) & 31] : cj + kWarps;
         }
         k0 = k1;
         w0 = w1;
@@ -1066,6 +1100,7 @@ __device__ __forceinline__ void bin_item2(const NetArgs<float>& a, const LayerDe
 template <typename T>
 struct LayerShared {
     SlotEntry<T> list[kWarps][32];
+    unsigned char cols[kWarps][32];  // map mode: the warp's columns the prune pass left
     int src[tile_rows<T>()];  // row compaction: source (tile * TR + row) of each new row
     int scan_c[2 * kWarps + 2];
     int count;
@@ -1074,6 +1109,92 @@ struct LayerShared {
     long long items;  // work items of the current layer
     int jb, nblk;     // outputs per item, items per tile
 };
+
+// Prune pass (sparse layers, one batch per column, bias < 0).  The per-column
+// test of layer_item gathers 32 metas from L2 for every (tile, column) -- 32
+// L1 wavefronts a column, the floor of a fully pruned layer (C4 layer 2:
+// 2.1 ms).  Here a work item is (tile, eighth of the outputs): the CTA
+// turns the tile's line bounds into 8-bit codes in shared memory (code =
+// ceil(bound / step), step = the tile's largest bound / 255 rounded up, so
+// code * step >= bound), then each warp walks its columns with the codes
+// coming from shared memory: the same rounded-up integer sum as layer_item's
+// test, one REDUX a column, one bit a column into the tile's prune map.
+// The coarser bound only ever prunes less; columns it leaves still get
+// layer_item's exact-bound test.  A tile holding a non-finite bound prunes
+// nothing.
+template <typename T>
+__device__ __forceinline__ void prune_pass(const NetArgs<T>& a, const LayerDesc<T>& L, int l, const int32_t* tiles,
+                                           int count, bool odd, unsigned char* codes, LayerShared<T>& sh) {
+    constexpr int PB = 8;  // output blocks per tile
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint2* imeta = odd ? a.meta[1] : a.meta[0];
+    const int words = (a.ld + 31) / 32;
+    const int groups = (a.n_out + 31) / 32, gblk = (groups + PB - 1) / PB;
+    const long long items = (long long)count * PB;
+    const float scale = prune_scale(L.bias);
+    const uint64_t wpol = policy_evict_last();
+    for (;;) {
+        if (tid == 0) sh.item = (long long)atomicAdd(&a.pp_work[l], 1u);
+        __syncthreads();
+        const long long it = sh.item;
+        __syncthreads();
+        if (it >= items) break;
+        const int t = tiles[(int)(it / PB)], bb = (int)(it % PB);
+        const uint2* m = imeta + (size_t)t * a.ld;
+        unsigned mx = 0u;
+#pragma unroll 8
+        for (int k = tid; k < a.n_in; k += kThreads) {
+            const uint2 e = m[k];
+            mx = max(mx, e.x ? e.y : 0u);
+        }
+        mx = __reduce_max_sync(0xffffffffu, mx);
+        if (lane == 0) sh.scan[warp] = (int)mx;
+        __syncthreads();
+        unsigned tm = 0u;
+        for (int w = 0; w < kWarps; ++w) tm = max(tm, (unsigned)sh.scan[w]);
+        const bool finite = tm < 0x7F800000u;
+        const float step = __fdiv_ru(__uint_as_float(tm), 255.f);
+        const float inv_step = __fdiv_ru(255.f, __uint_as_float(tm));  // NaN (tm = 0): unused, every bound is 0
+#pragma unroll 8
+        for (int k = tid; k < a.n_in; k += kThreads) {
+            const uint2 e = m[k];
+            const float bnd = e.x ? __uint_as_float(e.y) : 0.f;
+            codes[k] = bnd > 0.f ? (unsigned char)min(255u, __float2uint_ru(__fmul_ru(bnd, inv_step))) : (unsigned char)0;
+        }
+        __syncthreads();
+        uint32_t* map = a.prune_map + (size_t)t * words;
+        const int g1 = min(groups, (bb + 1) * gblk);
+        for (int g = bb * gblk + warp; g < g1; g += kWarps) {
+            unsigned word = 0u;
+            if (finite) {
+                const int cmax = min(32, a.n_out - g * 32);
+                constexpr int CU = 16;  // columns in flight per warp (the walk is latency-bound)
+                for (int c0 = 0; c0 < cmax; c0 += CU) {
+                    int k[CU];
+                    T w[CU];
+#pragma unroll
+                    for (int u = 0; u < CU; ++u) {
+                        const bool in = c0 + u < cmax;
+                        const size_t at = ((size_t)g * 32 + (in ? c0 + u : 0)) * 32 + lane;
+                        k[u] = ld_w(L.idx + at, wpol);
+                        w[u] = ld_w(L.val + at, wpol);
+                        if (!in) k[u] = -1;
+                    }
+#pragma unroll
+                    for (int u = 0; u < CU; ++u) {
+                        const float ub = k[u] >= 0 ? __fmul_ru((float)codes[k[u]], step) : 0.f;
+                        const float q = fminf(__fmul_ru(__fmul_ru(bound_up(w[u]), ub), scale), 67108864.f);
+                        if (__reduce_add_sync(0xffffffffu, __float2uint_ru(q)) <= 1048576u - 1024u)
+                            word |= 1u << (c0 + u);
+                    }
+                }
+                if (cmax < 32) word &= (1u << cmax) - 1u;
+            }
+            if (lane == 0) map[g] = word;
+        }
+        __syncthreads();  // the codes are rewritten by the next item
+    }
+}
 
 // One layer for this CTA: build the ascending live-tile list from the
 // layer's alive flags, then take (tile, output block) items in order from the
@@ -1110,7 +1231,9 @@ __device__ __forceinline__ void layer_pass(const NetArgs<T>& a, int l, int32_t* 
     const int count = sh.count;
     const LayerDesc<T> L = a.layers[l];
     int jb_l = a.jb;
-    if (a.jb_dense > 0 && a.jb_dense != a.jb && !BIN && count > 0) {
+    bool dense_in = false;
+    const bool want_pass = !BIN && a.prune_pass != 0 && a.prune != 0 && a.epilogue != 0 && L.wp == 32 && L.bias < T(0);
+    if (((a.jb_dense > 0 && a.jb_dense != a.jb) || want_pass) && !BIN && count > 0) {
         // the input's sector density picks the item width: every CTA samples
         // the same kDensitySample (tile, line) metas, so all decide alike
         const uint2* imeta = odd ? a.meta[1] : a.meta[0];
@@ -1126,7 +1249,17 @@ __device__ __forceinline__ void layer_pass(const NetArgs<T>& a, int l, int32_t* 
         int tot = 0;
         for (int w = 0; w < kWarps; ++w) tot += sh.scan[w];
         __syncthreads();
-        if ((long long)tot * 100 >= (long long)a.dense_pct * kDensitySample * 32) jb_l = a.jb_dense;
+        dense_in = (long long)tot * 100 >= (long long)a.dense_pct * kDensitySample * 32;
+        if (dense_in && a.jb_dense > 0) jb_l = a.jb_dense;
+    }
+    // sparse input: the prune pass first (every CTA decides alike), then a
+    // grid barrier so that every column's bit is in place before any item
+    const uint32_t* pmap = nullptr;
+    if (want_pass && count > 0 && !dense_in) {
+        extern __shared__ __align__(16) unsigned char dyn_smem[];
+        prune_pass<T>(a, L, l, tiles, count, odd, dyn_smem + a.pp_off, sh);
+        grid_barrier(a.bar, gridDim.x);
+        pmap = a.prune_map;
     }
     // the item width and item count live in shared memory, not in registers
     // across the item loop (the gather loop needs every register it has)
@@ -1154,7 +1287,9 @@ __device__ __forceinline__ void layer_pass(const NetArgs<T>& a, int l, int32_t* 
             bin_item2<GB>(a, L, tiles[ti], ti + 1 < count ? tiles[ti + 1] : -1, j0, j1,
                           reinterpret_cast<BinEntry2*>(sh.list[warp]));
         } else {
-            layer_item<T, GB, BIN, ZFILL>(a, L, l, odd, tiles[ti], j0, j1, sh.list[warp]);
+            layer_item<T, GB, BIN, ZFILL>(a, L, l, odd, tiles[ti], j0, j1, sh.list[warp],
+                                          pmap ? pmap + (size_t)tiles[ti] * ((a.ld + 31) / 32) : nullptr,
+                                          sh.cols[warp]);
         }
     }
 }
@@ -1696,7 +1831,7 @@ __device__ __forceinline__ void bin_quad_item1(const NetArgs<T>& a, const LayerD
 template <typename T>
 __host__ __device__ constexpr int prefilter_limit() { return sizeof(T) == 4 ? 32 : 160; }
 template <typename T>
-__global__ void __launch_bounds__(kThreads) quad_probe_kernel(NetArgs<T> a, int* flag) {
+__global__ void __launch_bounds__(kThreads) quad_probe_kernel(NetArgs<T> a, int* flag, int force) {
     constexpr int TPQ = quad_tiles<T>(), LPT = 32 / TPQ;
     __shared__ int s_sum[kWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1733,7 +1868,7 @@ __global__ void __launch_bounds__(kThreads) quad_probe_kernel(NetArgs<T> a, int*
     if (threadIdx.x == 0) {
         int tot = 0;
         for (int i = 0; i < kWarps; ++i) tot += s_sum[i];
-        *flag = (ok && tot <= prefilter_limit<T>() * 32) ? 1 : 0;
+        *flag = (ok && (force || tot <= prefilter_limit<T>() * 32)) ? 1 : 0;  // force: tests
     }
 }
 
