@@ -424,6 +424,11 @@ class DeviceArm:
                 "algorithmic_bytes": launch_bytes[dom],
                 "launch_ms": {"densify": round(float(stage_ms[0]), 3), "bin_layer": round(float(stage_ms[1]), 3),
                               "net": round(float(stage_ms[2]), 3)},
+                # every launch of the step against the same byte model
+                "launches": [{"kernel": names[i].split()[0], "ms": round(float(stage_ms[i]), 3),
+                              "algorithmic_bytes": launch_bytes[i],
+                              "frac": (launch_bytes[i] / (stage_ms[i] * 1e-3) / 1e9 / peak) if stage_ms[i] > 0 else 0.0}
+                             for i in range(3)],
                 "all_live_layers_gbs": all_gbs,
                 "live_layer_ms": [round(float(prof.layer_ms[l]), 3) for l in live_layers[:8]],
                 "peak_kind": peak_kind,
