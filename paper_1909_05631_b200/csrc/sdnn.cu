@@ -139,6 +139,10 @@ struct sdnn_net {
     int* probe_flag = nullptr;  // layer-1 walk chosen by quad_probe_kernel
     uint32_t* prune_map = nullptr;  // prune pass: one bit per (tile, output)
     int64_t pmcap = 0;
+    unsigned char* pp_codes = nullptr;  // prune pass: bound codes per tile
+    int64_t pccap = 0;
+    unsigned* pp_tmax = nullptr;
+    int64_t ptcap = 0;
     int32_t* tile_count = nullptr;
     int64_t* live_rows = nullptr;
     unsigned long long* stamps = nullptr;
@@ -635,7 +639,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
         if (int rc = grow(net->tile_count, c1, nl + 1, 4)) return rc;
         if (int rc = grow(net->live_rows, c2, nl + 1, 8)) return rc;
         if (int rc = grow(net->stamps, c3, nl + 1, 8)) return rc;
-        if (int rc = grow(net->work, c4, 4 * (nl + 1), 4)) return rc;  // layers, compactions, pruned columns, prune pass
+        if (int rc = grow(net->work, c4, 5 * (nl + 1), 4)) return rc;  // layers, compactions, pruned columns, prune pass x2
         net->lcap = nl + 1;
     }
     int32_t* tile_count = net->tile_count;
@@ -654,7 +658,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     uint32_t* heap = net->heap;
     CK(cudaMemsetAsync(heap, 0, (nl + 1) * tiles1 * 4, net->stream));
     unsigned* work = net->work;
-    CK(cudaMemsetAsync(work, 0, 4 * (nl + 1) * 4, net->stream));
+    CK(cudaMemsetAsync(work, 0, 5 * (nl + 1) * 4, net->stream));
     if (int rc = grow(net->alive_c, net->accap, tiles1 * AW, 4)) return rc;
     if (!net->n_compact) CK(cudaMalloc(&net->n_compact, 4));
     CK(cudaMemsetAsync(net->n_compact, 0, 4, net->stream));
@@ -717,13 +721,18 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
     {
         // prune pass: n_in bytes of bound codes behind the tile list, when that
         // keeps the kernel's CTAs per SM (SDNN_PRUNE_PASS=0: never)
-        const size_t pp_off = (smem + 15) / 16 * 16, with = pp_off + (size_t)n_in;
+        const size_t pp_off = (smem + 15) / 16 * 16, with = pp_off + (size_t)((ld + 15) / 16 * 16);
         int occ0 = 0, occ1 = 0;
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::min<size_t>(with, 200 << 10)));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ0, fn, kThreads, smem));
         if (with <= (200u << 10)) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, fn, kThreads, with));
         if (a.prune && env_int("SDNN_PRUNE_PASS", 1) != 0 && occ1 >= 1 && occ1 == occ0) {
             if (int rc = grow(net->prune_map, net->pmcap, tiles1 * ((ld + 31) / 32), 4)) return rc;
+            a.pp_ldc = (int)((ld + 15) / 16 * 16);
+            if (int rc = grow(net->pp_codes, net->pccap, tiles1 * a.pp_ldc, 1)) return rc;
+            if (int rc = grow(net->pp_tmax, net->ptcap, tiles1, 4)) return rc;
+            a.pp_codes = net->pp_codes;
+            a.pp_tmax = net->pp_tmax;
             a.prune_pass = 1;
             a.pp_off = (int)pp_off;
             a.prune_map = net->prune_map;
@@ -1545,6 +1554,8 @@ void sdnn_net_destroy(sdnn_net* net) {
     cudaFree(net->n_compact);
     cudaFree(net->probe_flag);
     cudaFree(net->prune_map);
+    cudaFree(net->pp_codes);
+    cudaFree(net->pp_tmax);
     cudaFree(net->rowlist);
     cudaFree(net->live_rows);
     cudaFree(net->stamps);

@@ -334,7 +334,10 @@ struct NetArgs {
     int prune_pass;       // 1: the launch has room for the codes (n_in bytes of dynamic shared memory)
     int pp_off;           // byte offset of the codes in dynamic shared memory
     uint32_t* prune_map;  // [n_tiles][(ld + 31) / 32] bit j: column j of the tile is pruned
-    unsigned* pp_work;    // [L] work-item counters of the pass
+    unsigned* pp_work;    // [2][L + 1] work-item counters of the pass (encode, walk)
+    unsigned char* pp_codes;  // [n_tiles][pp_ldc] a tile's bound codes (global staging for the bulk copy)
+    unsigned* pp_tmax;    // [n_tiles] the tile's largest bound (float bits)
+    int pp_ldc;           // bytes per tile of pp_codes: ld rounded up to 16
 };
 constexpr int kDensitySample = 256;  // input lines sampled per layer (the same ones in every CTA)
 
@@ -1138,6 +1141,8 @@ template <typename T>
 struct LayerShared {
     SlotEntry<T> list[kWarps][32];
     unsigned char cols[kWarps][32];  // map mode: the warp's columns the prune pass left
+    unsigned long long mbar;         // prune pass: completion barrier of the codes' bulk copy
+    unsigned pp_phase;               // its phase parity
     int src[tile_rows<T>()];  // row compaction: source (tile * TR + row) of each new row
     int scan_c[2 * kWarps + 2];
     int count;
@@ -1147,14 +1152,41 @@ struct LayerShared {
     int jb, nblk;     // outputs per item, items per tile
 };
 
+// Bulk asynchronous copy global -> shared memory (the TMA unit's non-tensor
+// path: cp.async.bulk, SASS UBLKCP) completing on an mbarrier.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    // earlier generic-proxy writes (other CTAs' codes, ordered by the grid
+    // barrier) before the async proxy reads them
+    asm volatile("fence.proxy.async;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@p bra DONE;\n\t"
+        "bra WAIT;\n\tDONE:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
 // Prune pass (sparse layers, one batch per column, bias < 0).  The per-column
 // test of layer_item gathers 32 metas from L2 for every (tile, column) -- 32
 // L1 wavefronts a column, the floor of a fully pruned layer (C4 layer 2:
-// 2.1 ms).  Here a work item is (tile, eighth of the outputs): the CTA
-// turns the tile's line bounds into 8-bit codes in shared memory (code =
+// 2.1 ms).  Here a tile's line bounds first become 8-bit codes (code =
 // ceil(bound / step), step = the tile's largest bound / 255 rounded up, so
-// code * step >= bound), then each warp walks its columns with the codes
-// coming from shared memory: the same rounded-up integer sum as layer_item's
+// code * step >= bound; one CTA a tile, written to global memory), and after
+// a grid barrier a work item is (tile, eighth of the outputs): one bulk
+// asynchronous copy (cp.async.bulk on an mbarrier, the TMA unit) brings the
+// tile's 64 KB of codes into shared memory, then each warp walks its columns
+// with the codes coming from shared memory: the same rounded-up integer sum as layer_item's
 // test, one REDUX a column, one bit a column into the tile's prune map.
 // The coarser bound only ever prunes less; columns it leaves still get
 // layer_item's exact-bound test.  A tile holding a non-finite bound prunes
@@ -1165,18 +1197,14 @@ __device__ __forceinline__ void prune_pass(const NetArgs<T>& a, const LayerDesc<
     constexpr int PB = 8;  // output blocks per tile
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint2* imeta = odd ? a.meta[1] : a.meta[0];
-    const int words = (a.ld + 31) / 32;
-    const int groups = (a.n_out + 31) / 32, gblk = (groups + PB - 1) / PB;
-    const long long items = (long long)count * PB;
-    const float scale = prune_scale(L.bias);
-    const uint64_t wpol = policy_evict_last();
+    // ---- encode: one item a tile, its bounds -> 8-bit codes in global memory
     for (;;) {
         if (tid == 0) sh.item = (long long)atomicAdd(&a.pp_work[l], 1u);
         __syncthreads();
         const long long it = sh.item;
         __syncthreads();
-        if (it >= items) break;
-        const int t = tiles[(int)(it / PB)], bb = (int)(it % PB);
+        if (it >= count) break;
+        const int t = tiles[(int)it];
         const uint2* m = imeta + (size_t)t * a.ld;
         unsigned mx = 0u;
 #pragma unroll 8
@@ -1189,16 +1217,38 @@ __device__ __forceinline__ void prune_pass(const NetArgs<T>& a, const LayerDesc<
         __syncthreads();
         unsigned tm = 0u;
         for (int w = 0; w < kWarps; ++w) tm = max(tm, (unsigned)sh.scan[w]);
-        const bool finite = tm < 0x7F800000u;
-        const float step = __fdiv_ru(__uint_as_float(tm), 255.f);
         const float inv_step = __fdiv_ru(255.f, __uint_as_float(tm));  // NaN (tm = 0): unused, every bound is 0
+        unsigned char* gc = a.pp_codes + (size_t)t * a.pp_ldc;
 #pragma unroll 8
         for (int k = tid; k < a.n_in; k += kThreads) {
             const uint2 e = m[k];
             const float bnd = e.x ? __uint_as_float(e.y) : 0.f;
-            codes[k] = bnd > 0.f ? (unsigned char)min(255u, __float2uint_ru(__fmul_ru(bnd, inv_step))) : (unsigned char)0;
+            gc[k] = bnd > 0.f ? (unsigned char)min(255u, __float2uint_ru(__fmul_ru(bnd, inv_step))) : (unsigned char)0;
         }
-        __syncthreads();
+        if (tid == 0) a.pp_tmax[t] = tm;
+        __syncthreads();  // sh.scan is rewritten by the next item
+    }
+    grid_barrier(a.bar, gridDim.x);
+    // ---- walk: (tile, eighth of the outputs); the tile's codes arrive in
+    // shared memory by one bulk copy
+    const int words = (a.ld + 31) / 32;
+    const int groups = (a.n_out + 31) / 32, gblk = (groups + PB - 1) / PB;
+    const long long items = (long long)count * PB;
+    const float scale = prune_scale(L.bias);
+    const uint64_t wpol = policy_evict_last();
+    unsigned ph = sh.pp_phase;
+    for (;;) {
+        if (tid == 0) sh.item = (long long)atomicAdd(&a.pp_work[a.L + 1 + l], 1u);
+        __syncthreads();  // (also: every warp is done with the previous item's codes)
+        const long long it = sh.item;
+        if (it >= items) break;
+        const int t = tiles[(int)(it / PB)], bb = (int)(it % PB);
+        if (tid == 0) bulk_load(codes, a.pp_codes + (size_t)t * a.pp_ldc, (unsigned)a.pp_ldc, &sh.mbar);
+        const unsigned tm = __ldcg(&a.pp_tmax[t]);
+        const bool finite = tm < 0x7F800000u;
+        const float step = __fdiv_ru(__uint_as_float(tm), 255.f);
+        mbar_wait(&sh.mbar, ph);
+        ph ^= 1u;
         uint32_t* map = a.prune_map + (size_t)t * words;
         const int g1 = min(groups, (bb + 1) * gblk);
         for (int g = bb * gblk + warp; g < g1; g += kWarps) {
@@ -1229,8 +1279,9 @@ __device__ __forceinline__ void prune_pass(const NetArgs<T>& a, const LayerDesc<
             }
             if (lane == 0) map[g] = word;
         }
-        __syncthreads();  // the codes are rewritten by the next item
     }
+    __syncthreads();
+    if (tid == 0) sh.pp_phase = ph;
 }
 
 // One layer for this CTA: build the ascending live-tile list from the
@@ -1292,7 +1343,33 @@ __device__ __forceinline__ void layer_pass(const NetArgs<T>& a, int l, int32_t* 
     // sparse input: the prune pass first (every CTA decides alike), then a
     // grid barrier so that every column's bit is in place before any item
     const uint32_t* pmap = nullptr;
-    if (want_pass && count > 0 && !dense_in) {
+    bool run_pass = want_pass && count > 0 && !dense_in;
+    if (run_pass) {
+        // worth a pass?  64 sampled (tile, column) pairs (the same in every
+        // CTA) through layer_item's exact-bound test: at least a quarter must
+        // prune (C1 / C2's layer 2 and a live layer prune nothing: no pass,
+        // no extra barriers)
+        const uint2* imeta = odd ? a.meta[1] : a.meta[0];
+        const float scale = prune_scale(L.bias);
+        int hits = 0;
+        for (int i = warp; i < 64; i += kWarps) {
+            const int t = tiles[(int)((((unsigned)i * 2654435761u) >> 4) % (unsigned)count)];
+            const int j = (int)((((unsigned)i * 40503u + 29u) * 2246822519u) % (unsigned)a.n_out);
+            const int k = L.idx[(size_t)j * 32 + lane];
+            const T w = L.val[(size_t)j * 32 + lane];
+            const uint2 m = k >= 0 ? imeta[(size_t)t * a.ld + k] : make_uint2(0u, 0u);
+            const float c = __fmul_ru(bound_up(w), __uint_as_float(m.y));
+            const float q = fminf(__fmul_ru(m.x ? c : 0.f, scale), 67108864.f);
+            hits += __reduce_add_sync(0xffffffffu, __float2uint_ru(q)) <= 1048576u - 1024u ? 1 : 0;
+        }
+        if (lane == 0) sh.scan[warp] = hits;
+        __syncthreads();
+        int tot = 0;
+        for (int w = 0; w < kWarps; ++w) tot += sh.scan[w];
+        __syncthreads();
+        run_pass = tot * 4 >= 64;
+    }
+    if (run_pass) {
         extern __shared__ __align__(16) unsigned char dyn_smem[];
         prune_pass<T>(a, L, l, tiles, count, odd, dyn_smem + a.pp_off, sh);
         grid_barrier(a.bar, gridDim.x);
@@ -2023,7 +2100,13 @@ __device__ __forceinline__ void compact_pass(const NetArgs<T>& a, int l, bool od
     uint2* ometa = odd ? a.meta[0] : a.meta[1];
     const int n_lines = l == 0 ? a.n_in : a.n_out;
     const int new_tiles = (total + TR - 1) / TR;
-    const int nblk = (n_lines + a.jb - 1) / a.jb;
+    // an item is (new tile, block of lines).  Every item rebuilds the tile's
+    // source map (a search per row, two block barriers), so blocks are as
+    // large as load balance allows: at least 8 a tile, enough for two items
+    // per CTA, at most one per a.jb lines
+    const int max_blk = (n_lines + a.jb - 1) / a.jb;
+    const int nblk = min(max_blk, max(8, (2 * (int)gridDim.x + new_tiles - 1) / new_tiles));
+    const int cjb = (n_lines + nblk - 1) / nblk;  // lines per block
     const long long items = (long long)new_tiles * nblk;
     // positions past the packed rows: no row, tile dead
     for (long long i = (long long)new_tiles * TR + (long long)blockIdx.x * kThreads + tid;
@@ -2073,9 +2156,24 @@ __device__ __forceinline__ void compact_pass(const NetArgs<T>& a, int l, bool od
         int src[RPL];
 #pragma unroll
         for (int c = 0; c < RPL; ++c) src[c] = sh.src[lane * RPL + c];
-        const int j0 = bb * a.jb, j1 = min(n_lines, j0 + a.jb);
+        const int j0 = bb * cjb, j1 = min(n_lines, j0 + cjb);
         const size_t tl_out = (size_t)nt * a.ld;
+        // the new tile's rows come, in ascending order, from the old tiles
+        // ot_lo .. ot_hi (usually two or three): lane i looks at old tile
+        // ot_lo + i's meta of a line first, and a line empty in all of them is
+        // empty in the new tile (sparse dying layers: almost every line)
+        const int n_new = min(TR, total - nt * TR);
+        const int ot_lo = sh.src[0] / TR, ot_hi = sh.src[n_new - 1] / TR;
+        const bool few = ot_hi - ot_lo < 32;
         for (int k = j0 + warp; k < j1; k += kWarps) {
+            if (few) {
+                const bool mine = ot_lo + lane <= ot_hi;
+                const unsigned mk = mine ? imeta[(size_t)(ot_lo + lane) * a.ld + k].x : 0u;
+                if (!__any_sync(0xffffffffu, mk != 0u)) {
+                    if (lane == 0) ometa[tl_out + k] = make_uint2(0u, 0u);
+                    continue;
+                }
+            }
             T v[RPL];
             unsigned bits = 0u;
 #pragma unroll
@@ -2121,7 +2219,11 @@ __global__ void __launch_bounds__(kThreads, SDNN_NET_OCC)
     // compactions so far (an odd count flips the slab parity); kept in
     // shared memory so the layer walk carries no extra register
     __shared__ int s_gen;
-    if (tid == 0) s_gen = 0;
+    if (tid == 0) {
+        s_gen = 0;
+        sh.pp_phase = 0u;
+        mbar_init(&sh.mbar, 1u);
+    }
     __syncthreads();
     for (int l = a.first_l; l < a.L; ++l) {
         // zero rows stay zero: once no tile is live every later layer is empty
