@@ -2165,15 +2165,8 @@ __device__ __forceinline__ void compact_pass(const NetArgs<T>& a, int l, bool od
         const int n_new = min(TR, total - nt * TR);
         const int ot_lo = sh.src[0] / TR, ot_hi = sh.src[n_new - 1] / TR;
         const bool few = ot_hi - ot_lo < 32;
-        for (int k = j0 + warp; k < j1; k += kWarps) {
-            if (few) {
-                const bool mine = ot_lo + lane <= ot_hi;
-                const unsigned mk = mine ? imeta[(size_t)(ot_lo + lane) * a.ld + k].x : 0u;
-                if (!__any_sync(0xffffffffu, mk != 0u)) {
-                    if (lane == 0) ometa[tl_out + k] = make_uint2(0u, 0u);
-                    continue;
-                }
-            }
+        // one line of the new tile from its rows' old sectors
+        auto move_line = [&](int k) {
             T v[RPL];
             unsigned bits = 0u;
 #pragma unroll
@@ -2195,6 +2188,33 @@ __device__ __forceinline__ void compact_pass(const NetArgs<T>& a, int l, bool od
             if (bits) st32(reinterpret_cast<char*>(out + (tl_out * 32 + hb + sector_pos(om, lane)) * RPL), v);
             const unsigned ob = om ? __reduce_max_sync(0xffffffffu, lane_bound(v)) : 0u;
             if (lane == 0) ometa[tl_out + k] = make_uint2(om, ob);
+        };
+        if (few) {
+            // eight lines' source metas in flight at once (the loop is bound
+            // by the latency of these loads when nearly every line is empty)
+            constexpr int LU = 8;
+            const bool mine = ot_lo + lane <= ot_hi;
+            const uint2* mp = imeta + (size_t)(ot_lo + (mine ? lane : 0)) * a.ld;
+            for (int k0 = j0 + warp; k0 < j1; k0 += LU * kWarps) {
+                unsigned mk[LU];
+#pragma unroll
+                for (int u = 0; u < LU; ++u) {
+                    const int k = k0 + u * kWarps;
+                    mk[u] = (mine && k < j1) ? mp[k].x : 0u;
+                }
+#pragma unroll
+                for (int u = 0; u < LU; ++u) {
+                    const int k = k0 + u * kWarps;
+                    if (k >= j1) break;
+                    if (__any_sync(0xffffffffu, mk[u] != 0u)) {
+                        move_line(k);
+                    } else if (lane == 0) {
+                        ometa[tl_out + k] = make_uint2(0u, 0u);
+                    }
+                }
+            }
+        } else {
+            for (int k = j0 + warp; k < j1; k += kWarps) move_line(k);
         }
         __syncthreads();  // sh.src / sh.item are rewritten by the next item
     }
