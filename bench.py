@@ -24,7 +24,10 @@ with Y0 resident in HBM, device time from CUDA events on the engine's
 stream.  `e2e`: the same metric through the C ABI with host buffers (the
 reference's int64/float64 CSR in, H2D of Y0 and D2H of the categories
 inside the timed region).  `roofline`: the dominant launch against
-measured HBM bandwidth.  `cpu_baseline` / `--impl reference`: the
+measured HBM bandwidth (`roofline.launches`: every launch of the step);
+`live.pruned_columns`: (tile, output) columns proven empty from their line
+bounds -- nothing is skipped unproven: every layer of every
+live tile is still visited, results are bit-identical with pruning off.  `cpu_baseline` / `--impl reference`: the
 UNMODIFIED reference engine (`sdnnbench.engine.infer_timed`, numba,
 data-parallel over every host core, float64) from `baseline/_ref` on a
 bounded sample of the same workload, extrapolated to the full batch (the
@@ -429,6 +432,9 @@ class DeviceArm:
                               "algorithmic_bytes": launch_bytes[i],
                               "frac": (launch_bytes[i] / (stage_ms[i] * 1e-3) / 1e9 / peak) if stage_ms[i] > 0 else 0.0}
                              for i in range(3)],
+                "launches_note": ("algorithmic bytes are the contract's dense byte model; a launch whose layers were "
+                                  "proven empty from their line bounds (live.pruned_columns) gathers nothing, so its "
+                                  "frac can exceed 1"),
                 "all_live_layers_gbs": all_gbs,
                 "live_layer_ms": [round(float(prof.layer_ms[l]), 3) for l in live_layers[:8]],
                 "peak_kind": peak_kind,
