@@ -733,7 +733,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
             if (int rc = grow(net->pp_tmax, net->ptcap, tiles1, 4)) return rc;
             a.pp_codes = net->pp_codes;
             a.pp_tmax = net->pp_tmax;
-            a.prune_pass = 1;
+            a.prune_pass = env_int("SDNN_PRUNE_PASS", 1) == 2 ? 2 : 1;
             a.pp_off = (int)pp_off;
             a.prune_map = net->prune_map;
             smem = with;

@@ -331,7 +331,8 @@ struct NetArgs {
     unsigned* pruned;     // [L] (tile, output) columns pruned per layer, or null
     // prune pass (sparse layers): a tile's line bounds as 8-bit codes in shared
     // memory, every column of the tile tested against them, one bit a column
-    int prune_pass;       // 1: the launch has room for the codes (n_in bytes of dynamic shared memory)
+    int prune_pass;       // 1: the launch has room for the codes (n_in bytes of dynamic shared memory); 2: and
+                          // the pass runs whatever the samples say (tests)
     int pp_off;           // byte offset of the codes in dynamic shared memory
     uint32_t* prune_map;  // [n_tiles][(ld + 31) / 32] bit j: column j of the tile is pruned
     unsigned* pp_work;    // [2][L + 1] work-item counters of the pass (encode, walk)
@@ -1343,8 +1344,8 @@ __device__ __forceinline__ void layer_pass(const NetArgs<T>& a, int l, int32_t* 
     // sparse input: the prune pass first (every CTA decides alike), then a
     // grid barrier so that every column's bit is in place before any item
     const uint32_t* pmap = nullptr;
-    bool run_pass = want_pass && count > 0 && !dense_in;
-    if (run_pass) {
+    bool run_pass = want_pass && count > 0 && (!dense_in || a.prune_pass == 2);
+    if (run_pass && a.prune_pass != 2) {  // (2: tests force the pass on every layer it applies to)
         // worth a pass?  64 sampled (tile, column) pairs (the same in every
         // CTA) through layer_item's exact-bound test: at least a quarter must
         // prune (C1 / C2's layer 2 and a live layer prune nothing: no pass,

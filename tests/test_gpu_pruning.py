@@ -188,3 +188,42 @@ def test_layer1_prefilter_with_uneven_weights(monkeypatch, dtype, prec, scale, b
         outs.append(r)
     assert np.array_equal(outs[0].live_rows, outs[2].live_rows)
     net.close()
+
+
+def test_forced_prune_pass_on_odd_sizes(monkeypatch):
+    """SDNN_PRUNE_PASS=2 runs the prune pass (bound codes by bulk copy into
+    shared memory, one bit per column) on every layer it applies to, whatever
+    the samples say: odd neuron counts (the bulk copy moves the codes rounded
+    up to 16 bytes), mixed-sign weights, live and dying rows, several tiles;
+    forced == default == oracle, float64 and float32."""
+    rng = np.random.default_rng(97)
+    forced_pruned = 0
+    for i in range(40):
+        n = int(rng.integers(17, 200))
+        layers, bias = [], []
+        for _ in range(int(rng.integers(2, 6))):
+            dens = rng.uniform(0.02, min(0.3, 30.0 / n))  # at most 32 per column (one batch of slots)
+            m = np.where(rng.random((n, n)) < dens, rng.uniform(-0.3, 1.0, (n, n)), 0.0)
+            while (m != 0).sum(axis=0).max() > 32:
+                m[:, (m != 0).sum(axis=0).argmax()] *= rng.random(n) < 0.5
+            layers.append(O.CSR.from_dense(m))
+            bias.append(float(rng.uniform(-0.9, -0.05)))
+        rows = int(rng.integers(1, 700))
+        y = (rng.random((rows, n)) < rng.uniform(0.05, 0.5)).astype(np.float64)
+        if i % 2:
+            y *= rng.uniform(0.05, 1.5, y.shape)
+        y0 = O.CSR.from_dense(y)
+        for dtype, prec in (("f64", 64), ("f32", 32)):
+            want = O.infer(layers, bias, y0, precision=prec)
+            net = E.DeviceNetwork(n, 0, dtype)
+            for m, b in zip(layers, bias):
+                net.add_layer_csr(sm(m), b)
+            batch = net.upload_csr(rows, y0.off, y0.cols, y0.vals)
+            for mode in ("2", "1"):
+                monkeypatch.setenv("SDNN_PRUNE_PASS", mode)
+                r = net.run(batch, 32.0, want_y=True)
+                assert O.CSR(rows, n, *r.y).identical(want), (i, dtype, mode)
+                if mode == "2":
+                    forced_pruned += r.pruned
+            net.close()
+    assert forced_pruned > 0
