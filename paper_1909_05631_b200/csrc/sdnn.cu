@@ -762,6 +762,21 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
             if (quad)  // group lines of dead neurons / missing tiles must read as zero
                 CK(cudaMemsetAsync(a.slab[0], 0, (size_t)((n_tiles + TPQ - 1) / TPQ) * ld * kQuadLine,
                                    net->stream));
+            if (quad && env_int("SDNN_DENSIFY_QUAD", 1) != 0) {
+                // a span of the tile's bit-lines in shared memory: float 1,024 lines (32 KB, four
+                // blocks per SM), double 2,048 lines (SDNN_QSPAN overrides; sweep in DESIGN.md)
+                const int qdef = sizeof(T) == 4 ? 1024 : 2048;
+                const int qspan = (int)std::min<int64_t>(std::max(32, env_int("SDNN_QSPAN", qdef) / 32 * 32),
+                                                         (n_in + 31) / 32 * 32);
+                const int64_t qblocks = n_tiles * ((n_in + qspan - 1) / qspan);
+                const size_t qsm = (size_t)qspan * (TR / 32) * 4;
+                CK(cudaFuncSetAttribute((const void*)densify_quad_kernel<T>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsm));
+                densify_quad_kernel<T><<<(int)std::min<int64_t>(qblocks, (int64_t)net->sm_count * 32), kDensifyThreads,
+                                         qsm, net->stream>>>(batch->off, batch->cols, batch->col_bytes, net->rowid,
+                                                             (int)n_in, (int)ld, (int)n_tiles, qspan, a.slab[0],
+                                                             a.meta[0], net->alive, tile_count);
+            } else {
             const int kcb = 1024;
             const int span = (int)(((n_in + spans - 1) / spans + kcb - 1) / kcb * kcb);
             const int64_t blocks = n_tiles * ((n_in + span - 1) / span);
@@ -772,6 +787,7 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
             densify_bin_kernel<T><<<dgrid, kDensifyThreads, bsmem, net->stream>>>(
                 batch->off, batch->cols, batch->col_bytes, net->rowid, (int)n_in, (int)ld, (int)n_tiles, kcb, span,
                 a.slab[0], a.meta[0], heap, net->alive, tile_count, quad ? 1 : 0);
+            }
         } else {
             const int span = (int)(((n_in + spans - 1) / spans + kc - 1) / kc * kc);
             const int64_t blocks = n_tiles * ((n_in + span - 1) / span);

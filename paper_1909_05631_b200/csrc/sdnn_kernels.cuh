@@ -674,6 +674,110 @@ __global__ void __launch_bounds__(kDensifyThreads) densify_bin_kernel(const int6
     }
 }
 
+// Binary Y0 -> quad / oct bit-lines with a whole span of lines in shared
+// memory (round 2).  densify_bin_kernel assembles 1,024-line chunks and spends
+// most of its instructions walking 16 row windows per warp per chunk round; here
+// a block owns (tile, span of lines) and keeps the span's bit-lines (float:
+// 1,024 lines x 32 bytes, four blocks per SM; double: 2,048 x 16 bytes) in
+// shared memory: one thread per row finds the row's first entry of the span by
+// binary search, then each warp streams its rows' entries (coalesced loads,
+// four in flight) and ORs one bit per entry into the span bitmap (word index
+// XOR-swizzled by the line, so the lanes' atomics spread over the banks);
+// finally one thread per line writes the tile's part of the 128-byte group
+// line and the line's liveness word.  C4: 1.36 -> 1.15 ms (float), 1.51 ->
+// 1.06 ms (double).  Measured and not kept: 4,096-line spans for float (128 KB,
+// one block per SM: 1.95 ms) and blocks that walk a group of consecutive spans
+// with the row cursors carried along (one search per group instead of per
+// span: 1.46 ms, fewer and longer blocks).
+template <typename T>
+__global__ void __launch_bounds__(kDensifyThreads) densify_quad_kernel(const int64_t* __restrict__ csr_off,
+                                                                       const void* __restrict__ csr_cols,
+                                                                       int col_bytes,
+                                                                       const int32_t* __restrict__ rowid, int n_in,
+                                                                       int ld, int n_tiles, int span, T* slab0,
+                                                                       uint2* meta0, uint32_t* alive0,
+                                                                       int32_t* tile_count0) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    constexpr int TR = tile_rows<T>(), AW = alive_words<T>(), W = TR / 32;  // words per bit-line
+    constexpr int NW = kDensifyThreads / 32, TPQ = 32 / W;
+#ifndef SDNN_QLOADS
+#define SDNN_QLOADS 4
+#endif
+    constexpr int QL = SDNN_QLOADS;  // coalesced loads of a row in flight
+    uint32_t* bm = reinterpret_cast<uint32_t*>(dsm);  // [span][W]
+    __shared__ int64_t s_pos[TR], s_end[TR];
+    __shared__ uint32_t s_alive[AW];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n_spans = (n_in + span - 1) / span;
+    for (int bb = blockIdx.x; bb < n_tiles * n_spans; bb += gridDim.x) {
+        const int t = bb / n_spans;
+        const int kbeg = (bb % n_spans) * span, kend = min(n_in, kbeg + span), kn = kend - kbeg;
+        for (int i = tid; i < kn * W; i += blockDim.x) bm[i] = 0u;
+        if (tid < AW) s_alive[tid] = 0u;
+        __syncthreads();
+        for (int r = tid; r < TR; r += blockDim.x) {
+            const int row = rowid[(size_t)t * TR + r];
+            const int64_t p = row >= 0 ? csr_off[row] : 0, e = row >= 0 ? csr_off[row + 1] : 0;
+            if (e > p) {
+                atomicOr(&s_alive[r / 32], 1u << (r % 32));
+                atomicOr(&s_alive[AW - 1], 1u);
+            }
+            int64_t lo = p, hi = e;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (load_col(csr_cols, col_bytes, mid) < kbeg) lo = mid + 1;
+                else hi = mid;
+            }
+            s_pos[r] = lo;
+            s_end[r] = e;
+        }
+        __syncthreads();
+        for (int r = warp; r < TR; r += NW) {
+            const int64_t e = s_end[r];
+            const uint32_t bit = 1u << (r & 31);
+            const int wofs = r >> 5;
+            for (int64_t q = s_pos[r] + lane;; q += 32 * QL) {
+                int col[QL];
+#pragma unroll
+                for (int u = 0; u < QL; ++u)
+                    col[u] = q + 32 * u < e ? load_col(csr_cols, col_bytes, q + 32 * u) : INT32_MAX;
+#pragma unroll
+                for (int u = 0; u < QL; ++u)
+                    if (col[u] < kend) {
+                        const int kk = col[u] - kbeg;
+                        atomicOr(&bm[kk * W + (wofs ^ bin_swz<W>(kk))], bit);
+                    }
+                // entries ascend: once a lane's last one is past the span (or the row), the row is done
+                if (!__all_sync(0xffffffffu, col[QL - 1] < kend)) break;
+            }
+        }
+        __syncthreads();
+        for (int k = tid; k < kn; k += blockDim.x) {
+            uint32_t wv[W];
+            uint32_t any = 0u;
+#pragma unroll
+            for (int q = 0; q < W; ++q) {
+                wv[q] = bm[k * W + (q ^ bin_swz<W>(k))];
+                any |= wv[q];
+            }
+            if (any) {
+                uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<char*>(slab0) +
+                                                      ((size_t)(t / TPQ) * ld + (kbeg + k)) * 128 + (t % TPQ) * (W * 4));
+                dst[0] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                if constexpr (W == 8) dst[1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
+                // one liveness word per (group, line): every tile of the group that
+                // holds the line writes the same value
+                meta0[(size_t)(t / TPQ) * ld + (kbeg + k)] = make_uint2(0xFFFFFFFFu, (unsigned)(kbeg + k));
+            }
+        }
+        __syncthreads();
+        if (tid < AW - 1 && s_alive[tid]) atomicOr(&alive0[(size_t)t * AW + tid], s_alive[tid]);
+        if (tid == AW - 1 && s_alive[tid] && atomicOr(&alive0[(size_t)t * AW + tid], 1u) == 0u)
+            atomicAdd(tile_count0, 1);
+        __syncthreads();
+    }
+}
+
 // ------------------------------------------------------------ one item
 // Output columns [j0, j1) of tile t for layer l: warp per column.
 // The warp walks its columns' 32-slot batches with a three-stage prefetch
