@@ -377,7 +377,7 @@ class DeviceArm:
         rd0 = float(self.nnz0 * (4 + elem) + (self.rows + 1) * 8) if prof.live_rows[0] > 0 else 0.0
         launch_bytes = [rd0 if bin_first else 0.0, float(lb[0]) - rd0 if bin_first else 0.0,
                         float(lb[1:].sum() if bin_first else lb.sum())]
-        names = ["densify_bin_kernel (Y0 -> bit-line tiles)" if bin_first else "densify_kernel (Y0 -> tiles)",
+        names = ["densify_quad_kernel (Y0 -> bit-line tiles)" if bin_first else "densify_kernel (Y0 -> tiles)",
                  "bin_quad_kernel (layer 1, quad/oct bit-lines)",
                  f"net_kernel (layers {2 if bin_first else 1}-{w.layers}, persistent)"]
         dom = int(np.argmax(stage_ms))

@@ -10,6 +10,6 @@ timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --
    --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --companions '' --no-cpu > gpurun_out/launch_ncu.log 2>&1
 echo "launch list exit $?"
 ARGS="--steps 1 --warmup 1 --companions '' --no-cpu"
-eval timeout 2400 ncu --set full --clock-control none --import-source on -k regex:'net_kernel\|bin_quad_kernel\|densify_bin' -c 5 \
+eval timeout 2400 ncu --set full --clock-control none --import-source on -k regex:'net_kernel\|bin_quad_kernel\|densify_bin\|densify_quad' -c 5 \
     -o gpurun_out/full_c4 python bench.py $ARGS > gpurun_out/full_c4_ncu.log 2>&1
 echo "ncu full exit $?"
