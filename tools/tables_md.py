@@ -17,8 +17,9 @@ R01_SWEEP = {(1000, 0.1): 0.296, (1000, 0.35): 0.665, (1000, 0.7): 1.136, (15000
              (15000, 0.7): 11.234, (60000, 0.1): 12.910, (60000, 0.35): 24.072, (60000, 0.7): 47.657,
              (240000, 0.1): 50.917, (240000, 0.35): 95.496, (240000, 0.7): 196.010}
 
-shutil.copy(cfg_path, prof / f"{tag}_configs.jsonl")
-shutil.copy(sweep_path, prof / f"{tag}_c5_sweep.jsonl")
+for src, dst in ((cfg_path, prof / f"{tag}_configs.jsonl"), (sweep_path, prof / f"{tag}_c5_sweep.jsonl")):
+    if Path(src).resolve() != dst.resolve():
+        shutil.copy(src, dst)
 out = [f"# {tag}: every BASELINE config through bench.py (--steps 5 --warmup 3 --companions '' --no-cpu; "
        "tools/gpu_configs.sh), one B200, final kernels (output pruning, prune pass, layer-1 probe: defaults)",
        "# (r01's first column started at the densify kernel; since round 2 the device time starts at the live-row "
