@@ -762,7 +762,13 @@ int run_wave(sdnn_net* net, const sdnn_batch* batch, double ymax, int64_t first,
             if (quad)  // group lines of dead neurons / missing tiles must read as zero
                 CK(cudaMemsetAsync(a.slab[0], 0, (size_t)((n_tiles + TPQ - 1) / TPQ) * ld * kQuadLine,
                                    net->stream));
-            if (quad && env_int("SDNN_DENSIFY_QUAD", 1) != 0) {
+            // densify_quad_kernel pays one row search per (tile, span): it wins once rows are
+            // at least ~6 % dense (C5 p = 0.35: 1.36 -> 1.15 ms, p = 0.7: 2.3 -> 1.8 ms; p = 0.1,
+            // 3.9 % dense: 0.68 -> 0.79 ms, so sparser batches keep the chunked kernel);
+            // SDNN_DENSIFY_QUAD=0 never, 2 always
+            const int dq = env_int("SDNN_DENSIFY_QUAD", 1);
+            const bool dense_rows = batch->nnz * 16 >= std::max<int64_t>(batch->n_rows, 1) * n_in;
+            if (quad && (dq == 2 || (dq == 1 && dense_rows))) {
                 // a span of the tile's bit-lines in shared memory: float 1,024 lines (32 KB, four
                 // blocks per SM), double 2,048 lines (SDNN_QSPAN overrides; sweep in DESIGN.md)
                 const int qdef = sizeof(T) == 4 ? 1024 : 2048;

@@ -739,3 +739,35 @@ def _ell_csr(idx, n, value):
                                                   _lib.ptr(np.full(idx.size, value)), _lib.ptr(off),
                                                   _lib.ptr(cols), _lib.ptr(vals)))
     return off, cols, vals
+
+
+@pytest.mark.parametrize("dtype,prec", [("f64", 64), ("f32", 32)])
+@pytest.mark.parametrize("n,rows,p", [(1024, 700, 0.35), (4096, 300, 0.05), (1000, 513, 0.7)])
+def test_both_bit_line_builders_agree(env, n, rows, p, dtype, prec):
+    """Binary Y0 -> quad / oct bit-lines by densify_quad_kernel (a span of
+    lines in shared memory, one row stream per warp: SDNN_DENSIFY_QUAD=2) and
+    by densify_bin_kernel (0); the default picks by row density.  Same bits,
+    equal to the oracle, for dense, sparse and ragged batches (empty rows,
+    a neuron count that is no multiple of 32, a last tile with few rows)."""
+    rng = np.random.default_rng(n + rows)
+    layers, bias = [], []
+    for _ in range(3):
+        m = np.zeros((n, n))
+        for j in range(n):
+            m[rng.choice(n, 24, replace=False), j] = rng.uniform(0.05, 0.2, 24)
+        layers.append(O.CSR.from_dense(m))
+        bias.append(-0.3)
+    y = (rng.random((rows, n)) < p).astype(np.float64)
+    y[rng.choice(rows, rows // 7, replace=False)] = 0.0  # empty rows never enter a tile
+    y0 = O.CSR.from_dense(y)
+    want = O.infer(layers, bias, y0, precision=prec, threads=8)
+    net = E.DeviceNetwork(n, 0, dtype)
+    for m, b in zip(layers, bias):
+        net.add_layer_csr(sm(m), b)
+    batch = net.upload_csr(rows, y0.off, y0.cols, y0.vals)
+    for mode in ("2", "0", "1"):
+        env["SDNN_DENSIFY_QUAD"] = mode
+        r = net.run(batch, 32.0, want_y=True)
+        assert O.CSR(rows, n, *r.y).identical(want), (mode, dtype)
+        assert np.array_equal(r.categories, O.categorize(want)), (mode, dtype)
+    net.close()
